@@ -1,0 +1,219 @@
+/*
+ * lsgpu.h -- C ABI of liblsgpu.so, the B200 (sm_100a) hot path of the
+ * level-set compliance loop.
+ *
+ * The reference (lsopt 0.1.0, /root/reference/pkg/src/lsopt) is pure
+ * Python/numpy/scipy and has no C ABI; its drop-in seams are the Python
+ * functions listed beside each entry point below.
+ * The package paper_2601_05709_b200 binds these symbols through ctypes and
+ * re-exposes the reference's Python entry points on top of them.
+ *
+ * Conventions
+ *   - Every array is a caller-owned DEVICE pointer (fp64 unless stated).
+ *     Nothing in the library allocates device memory.
+ *   - Vector fields interleave components, dof = dim*node + c, exactly like
+ *     the reference (fem.py:88-96); a batch of k fields is k contiguous
+ *     vectors of dim*N doubles.
+ *   - Node numbering is the reference's: 2D vid = j*(nx+1)+i (mesh.py:137),
+ *     3D vid = (k*(ny+1)+j)*(nx+1)+i.
+ *   - `stream` is a cudaStream_t passed as void*; NULL = legacy default
+ *     stream.  Calls only enqueue work; none synchronises the device.
+ *   - Return value 0 = success, <0 = error; lsg_last_error() returns a
+ *     thread-local message.  LSG_ERR_ARG maps to ConfigError, LSG_ERR_CUDA
+ *     to RuntimeError on the Python side.
+ *   - Reductions are deterministic (fixed-order two-level sums, no float
+ *     atomics): identical inputs give bitwise-identical outputs.
+ */
+#ifndef LSGPU_H
+#define LSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSG_OK 0
+#define LSG_ERR_ARG -1
+#define LSG_ERR_CUDA -2
+
+/* Structured box mesh [lo, hi] with n[a] cells per axis; dim = 2 (right
+ * triangles split along the lower-left/upper-right diagonal, mesh.py:140-150)
+ * or 3 (six Kuhn tetrahedra per hexahedron). n[2], lo[2], hi[2] are ignored
+ * when dim == 2. */
+typedef struct {
+  int32_t dim;
+  int32_t n[3];
+  double lo[3];
+  double hi[3];
+} lsg_grid;
+
+/* Operator kinds for lsg_op. */
+#define LSG_OP_ELASTICITY 1 /* ersatz-material linear elasticity (fem.py:397-411) */
+#define LSG_OP_H1 2         /* velocity form, velocity.py:98-127 */
+
+/* Matrix-free operator description.
+ *   ELASTICITY: words = per-node material word written by lsg_material
+ *               (uint8 in 2D, uint32 in 3D); p0 = lambda, p1 = mu,
+ *               p2 = outside (ersatz) coefficient, p3 = inside coefficient
+ *               (MaterialIndicator(inside, outside), base.py:100-121;
+ *               0 is read as 1), p4..p5 unused.
+ *   H1:         words = per-node form word written by lsg_h1_words;
+ *               p0 = mass_weight, p1 = stiffness_weight,
+ *               p2 = boundary_normal_penalty, p3 = frozen_penalty.
+ * Dirichlet dofs (bits in the words) are eliminated symmetrically:
+ *   y = m.*A(m.*x) + (1-m).*x (fem.py:274-291). */
+typedef struct {
+  int32_t kind;
+  int32_t pad_;
+  lsg_grid grid;
+  const void *words;
+  double p[6];
+} lsg_op;
+
+/* Per right-hand-side PCG scalars (device memory, 16 doubles each). */
+typedef struct {
+  double atol;     /* max(atol, rtol*||b||) -- scipy cg stopping threshold */
+  double rho;      /* r.z of the current iterate */
+  double alpha;
+  double beta;
+  double rr;       /* ||r||^2 (recursive residual) */
+  double pq;
+  double bb;       /* ||b||^2 */
+  double iters;    /* completed iterations */
+  double done;     /* 1 once ||r|| < atol (or b == 0) */
+  double zero_rhs; /* 1 if b == 0: x is returned as b (scipy cg semantics) */
+  double maxiter;
+  double first;    /* 1 until the first p = z has been formed */
+  double rz_new;
+  double reserved[3];
+} lsg_pcg_scalars;
+
+/* PCG workspace; every pointer is device memory owned by the caller.
+ *   x, b, r, p, q : k * n doubles each (n = dim * num_nodes)
+ *   scal          : k lsg_pcg_scalars
+ *   partials      : k * lsg_partials_per_rhs() * 4 doubles
+ *   counters      : k uint32, zero-initialised once by the caller */
+typedef struct {
+  int32_t k;
+  int32_t pad_;
+  double *x;
+  const double *b;
+  double *r;
+  double *p;
+  double *q;
+  lsg_pcg_scalars *scal;
+  double *partials;
+  uint32_t *counters;
+} lsg_pcg_ws;
+
+int32_t lsg_abi_version(void);
+const char *lsg_last_error(void);
+/* Number of kernels this library has launched in the process so far. */
+int64_t lsg_launch_count(void);
+
+/* Number of nodes / elements / blocks-per-rhs used by the reductions. */
+int64_t lsg_num_nodes(const lsg_grid *g);
+int64_t lsg_num_elements(const lsg_grid *g);
+int64_t lsg_partials_per_rhs(const lsg_grid *g);
+
+/* Mesh generation on the device -- replaces build_rect_mesh's arrays
+ * (mesh.py:132-150): xyz (N, dim) coordinates bit-identical to np.linspace,
+ * conn (E, dim+1) int32 element connectivity in the reference order. */
+int lsg_mesh_vertices(const lsg_grid *g, double *xyz, void *stream);
+int lsg_mesh_elements(const lsg_grid *g, int32_t *conn, void *stream);
+
+/* Material words from the level set -- replaces MaterialIndicator.at_quad
+ * + LevelSetField.indicator_quad (models/base.py:117-119, levelset.py:65-67).
+ * phi: N doubles; bcmask: N bytes (bit c = Dirichlet on component c);
+ * words: N uint8 (2D) / uint32 (3D). */
+int lsg_material(const lsg_grid *g, const double *phi, const uint8_t *bcmask,
+                 void *words, void *stream);
+
+/* Per-quadrature-point indicator chi (E, nq) as doubles, for parity checks
+ * against LevelSetField.indicator_quad (levelset.py:65-67). */
+int lsg_indicator_quad(const lsg_grid *g, const double *phi, double *chi, void *stream);
+
+/* Velocity-form words (H1 operator): frozen quadrature bits and the
+ * zero-Dirichlet flag.  frozen_q: (E, nq) bytes (nonzero = inside the frozen
+ * subdomain) or NULL; zero_dirichlet pins every boundary node. */
+int lsg_h1_words(const lsg_grid *g, const uint8_t *frozen_q, int32_t zero_dirichlet,
+                 void *words, void *stream);
+
+/* y = A x for k stacked vectors -- replaces the CSR product K @ u of the
+ * assembled, Dirichlet-eliminated operator (fem.py:141-150, 274-291). */
+int lsg_apply(const lsg_op *op, int32_t k, const double *x, double *y, void *stream);
+
+/* Jacobi diagonal of the eliminated operator (fem.py:303-305), n doubles. */
+int lsg_diag(const lsg_op *op, double *diag, void *stream);
+
+/* Batched Jacobi-PCG with scipy cg semantics (fem.py:294-316 via
+ * scipy.sparse.linalg.cg): stop when ||r|| < max(atol, rtol*||b||), checked
+ * before each iteration; b == 0 returns x = b.  x holds the warm start on
+ * entry.  lsg_pcg_start computes r = b - A x and the stopping thresholds;
+ * lsg_pcg_iterate enqueues `niter` more iterations (two fused kernels each);
+ * converged right-hand sides freeze.  Poll ws->scal (done, iters). */
+int lsg_pcg_start(const lsg_op *op, const lsg_pcg_ws *ws, double rtol, double atol,
+                  double maxiter, void *stream);
+int lsg_pcg_iterate(const lsg_op *op, const lsg_pcg_ws *ws, int32_t niter, void *stream);
+
+/* Fused compliance evaluation + shape-derivative right-hand side --
+ * replaces ComplianceModel.cost/constraint/derivative (compliance.py:111-139,
+ * base.py:150-158) + VelocitySolver._derivative_vector (velocity.py:129-142):
+ *   vec_cost_a = sum_e |e| abar_e bulk_e grad N_a,
+ *                bulk_e = sum_k (2 G_k^T sigma_k - (sigma_k:eps_k) I)
+ *   vec_vol_a  = sum_e |e| (n_in/nq) / V grad N_a
+ *   out[0] = J = sum_k sum_e |e| abar_e sigma_k:eps_k ; out[1] = int chi.
+ * u: k fields; words from lsg_material; out: 2 doubles (device).
+ * s1: reserved, pass NULL (the tensor itself never touches memory on the hot
+ * path; lsg_s1_tensor materialises it for parity checks).
+ * partials: lsg_partials_per_rhs() x 4 doubles; counter: one zero-initialised
+ * uint32. */
+int lsg_shape_rhs(const lsg_op *op, int32_t k, const double *u, double volume,
+                  double *vec_cost, double *vec_vol, double *out, double *s1,
+                  double *partials, uint32_t *counter, void *stream);
+
+/* S1 of the cost per element and quadrature point, (E, nq, dim, dim), for
+ * parity with ComplianceModel.derivative's tensor (compliance.py:128-139):
+ * S1_q = A_q sum_k (2 G_k^T sigma_k - (sigma_k:eps_k) I), A_q from phi. */
+int lsg_s1_tensor(const lsg_op *op, int32_t k, const double *u, const double *phi, double *s1,
+                  void *stream);
+
+/* Generic tensor pair -> derivative vector (velocity.py:129-142):
+ * vec_(a,c) = sum_q w_q (S0_q[c] N_a(x_q) + S1_q[c,:] . grad N_a);
+ * s0: (E,nq,dim) or NULL, s1: (E,nq,dim,dim) or NULL. */
+int lsg_tensor_rhs(const lsg_grid *g, const double *s0, const double *s1, double *vec,
+                   void *stream);
+
+/* b = -(vec_cost + lam * vec_vol), with Dirichlet dofs of the H1 operator
+ * zeroed (velocity.py:144-148). */
+int lsg_velocity_rhs(const lsg_op *h1, const double *vec_cost, const double *vec_vol,
+                     double lam, double *b, void *stream);
+
+/* Velocity statistics after the H1 solve (velocity.py:149-154):
+ * out[0] = theta^T B theta, out[1] = vec . theta (vec = -b on free dofs,
+ * passed explicitly), out[2] = max_i sum_d |theta_d,i| / h_d (CFL speed).
+ * partials/counter as for lsg_shape_rhs. */
+int lsg_velocity_stats(const lsg_op *h1, const double *theta, const double *vec,
+                       double *out, double *partials, uint32_t *counter, void *stream);
+
+/* Explicit level-set update (north star (4); replaces levelset.transport /
+ * reinitialize, levelset.py:137-216).  Both run `nsub` forward-Euler
+ * substeps of size dt, ping-ponging between phi_out and tmp; the result is in
+ * phi_out.  transport: conservative face-velocity upwind + [smooth] h^2 lap.
+ * reinit: Godunov, frozen S = phi0/sqrt(phi0^2+h^2) (sgn: N doubles scratch). */
+int lsg_transport(const lsg_grid *g, const double *phi_in, const double *theta, double dt,
+                  int32_t nsub, int32_t smooth, double h, double *phi_out, double *tmp,
+                  void *stream);
+int lsg_reinit(const lsg_grid *g, const double *phi_in, double dt, int32_t nsub, double h,
+               double *phi_out, double *tmp, double *sgn, void *stream);
+
+/* max_i sum_d |v_d,i| / h_d over a vector field (CFL speed), out: 1 double. */
+int lsg_cfl_speed(const lsg_grid *g, const double *v, double *out, double *partials,
+                  uint32_t *counter, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSGPU_H */

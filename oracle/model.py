@@ -1,0 +1,210 @@
+"""Compliance model, velocity solve and PPL multipliers (oracle; test infrastructure only).
+
+Restates, dimension-generically:
+
+* ``MaterialIndicator.at_quad`` (reference ``models/base.py:100-121``):
+  A_q = chi_q + ersatz (1 - chi_q), chi_q = [phi(x_q) < 0];
+* ``ComplianceModel`` / ``CompliancePlusModel`` (``models/compliance.py:37-156``):
+  one shared elasticity operator for all loads (``:97-106``), adjoint -2u
+  (``:108-109``), J = sum_k int A sigma_k : eps_k (``:111-123``),
+  C = int chi / V (``base.py:150-152``), S1 = A sum_k (2 G_k^T sigma_k -
+  (sigma_k : eps_k) I) (``:128-139``) plus the multiplier-weighted volume
+  tensor lam chi/V I (``base.py:155-158``, ``ppl.py:66-97``);
+* ``VelocitySolver`` (``velocity.py:91-154``): B = mass_w M + stiff_w K
+  (+ boundary-normal penalty, + frozen mass, + zero Dirichlet), RHS
+  vec_a = int S0 . N_a + S1 : grad(N_a e_c), theta = B^-1 (-vec),
+  form_value = theta^T B theta, derivative = vec . theta;
+* PPL recursion and Lagrangian (``ppl.py:47-63,100-114``).
+"""
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from . import fem
+
+
+class Compliance:
+    def __init__(self, grid, lame, ersatz, clamp_dofs, loads, volume):
+        self.grid = grid
+        self.space = fem.Space(grid, grid.dim)
+        self.scalar = fem.Space(grid, 1)
+        self.lame = tuple(float(v) for v in lame)
+        self.ersatz = float(ersatz)
+        self.clamp = np.asarray(clamp_dofs, dtype=np.int64)
+        self.loads = [np.asarray(b, dtype=float) for b in loads]
+        self.volume = float(volume)
+
+    # -- material -----------------------------------------------------------------
+    def chi(self, phi):
+        return fem.phi_at_quad_sign(self.space, phi).astype(float)
+
+    def a_q(self, phi):
+        chi = self.chi(phi)
+        return chi + self.ersatz * (1.0 - chi)
+
+    # -- state ----------------------------------------------------------------------
+    def matrix(self, phi):
+        return self.space.assemble_matrix(fem.elasticity_elements(self.space, self.a_q(phi), self.lame))
+
+    def eliminated(self, phi):
+        K = self.matrix(phi)
+        out = []
+        for b in self.loads:
+            A, rhs = fem.dirichlet_eliminate(K, b, self.clamp)
+            out.append((A, rhs))
+        return out
+
+    def solve_states(self, phi, warm=None, rtol=fem.CG_RTOL):
+        states, iters = [], []
+        for k, (A, b) in enumerate(self.eliminated(phi)):
+            x0 = None if warm is None else warm[k]
+            x, it = fem.jacobi_pcg(A, b, x0=x0, rtol=rtol)
+            states.append(x)
+            iters.append(it)
+        return states, iters
+
+    # -- functionals ----------------------------------------------------------------
+    def energy(self, u):
+        jac = self.space.grad_at_quad(u)
+        eps = fem.strain(jac)
+        sig = fem.stress(eps, self.lame)
+        return jac, sig, np.einsum("tij,tij->t", sig, eps)
+
+    def cost(self, phi, states):
+        a_q = self.a_q(phi)
+        total = 0.0
+        for u in states:
+            dens = self.energy(u)[2]
+            total += float(np.sum(self.space.quad_weights * (a_q * dens[:, None])))
+        return total
+
+    def constraint(self, phi):
+        return float(np.sum(self.space.quad_weights * self.chi(phi))) / self.volume
+
+    def s1_cost(self, phi, states):
+        a_q = self.a_q(phi)
+        d = self.grid.dim
+        s1 = np.zeros(a_q.shape + (d, d))
+        for u in states:
+            jac, sig, dens = self.energy(u)
+            bulk = 2.0 * np.einsum("tki,tkj->tij", jac, sig) - dens[:, None, None] * np.eye(d)
+            s1 += a_q[:, :, None, None] * bulk[:, None, :, :]
+        return s1
+
+    def s1_volume(self, phi):
+        return self.chi(phi)[:, :, None, None] * (np.eye(self.grid.dim) / self.volume)
+
+    def s1_combined(self, phi, states, lam):
+        return self.s1_cost(phi, states) + lam * self.s1_volume(phi)
+
+
+def derivative_vector(space, s1=None, s0=None):
+    """vec_(a,c) = int S0_c N_a + S1[c,:] . grad N_a (reference ``velocity.py:129-142``)."""
+    vec = np.zeros(space.dof_count)
+    n_el = len(space.grads)
+    if s0 is not None:
+        elems = np.einsum("tq,tqc,qa->tac", space.quad_weights, s0, space.bary)
+        vec += space.assemble_vector(elems.reshape(n_el, -1))
+    if s1 is not None:
+        elems = np.einsum("tq,tqcd,tad->tac", space.quad_weights, s1, space.grads)
+        vec += space.assemble_vector(elems.reshape(n_el, -1))
+    return vec
+
+
+def facet_normal_axes(grid):
+    """Outward normal of each boundary facet of the box as (axis, sign)."""
+    mids = grid.facet_midpoints()
+    axes = np.zeros(len(mids), dtype=np.int64)
+    signs = np.zeros(len(mids))
+    for a in range(grid.dim):
+        lo = np.isclose(mids[:, a], grid.lo[a], rtol=0, atol=1e-12 * (grid.hi[a] - grid.lo[a]))
+        hi = np.isclose(mids[:, a], grid.hi[a], rtol=0, atol=1e-12 * (grid.hi[a] - grid.lo[a]))
+        axes[lo | hi] = a
+        signs[lo] = -1.0
+        signs[hi] = 1.0
+    return axes, signs
+
+
+class Velocity:
+    """H1-type velocity form, solved by sparse LU (reference ``velocity.py:98-127``)."""
+
+    def __init__(self, grid, mass_weight=1.0, stiffness_weight=1e-2,
+                 boundary_normal_penalty=0.0, frozen_chi=None, frozen_penalty=0.0,
+                 zero_dirichlet=False):
+        self.grid = grid
+        self.space = fem.Space(grid, grid.dim)
+        sp_ = self.space
+        elems = stiffness_weight * fem.stiffness_elements(sp_)
+        if mass_weight > 0:
+            elems = elems + mass_weight * fem.mass_elements(sp_)
+        if frozen_chi is not None and frozen_penalty > 0:
+            elems = elems + frozen_penalty * fem.mass_elements(sp_, frozen_chi)
+        B = sp_.assemble_matrix(elems)
+        if boundary_normal_penalty > 0:
+            B = B + boundary_normal_penalty * self._normal_matrix()
+        self.form_matrix = B.tocsr()
+        self.bc = None
+        solvable = self.form_matrix
+        if zero_dirichlet:
+            self.bc = fem.clamp_dofs(sp_, np.arange(len(grid.boundary_facets)))
+            solvable, _ = fem.dirichlet_eliminate(self.form_matrix, np.zeros(sp_.dof_count), self.bc)
+        self.lu = spla.splu(solvable.tocsc())
+
+    def _normal_matrix(self):
+        grid, d = self.grid, self.grid.dim
+        facets = grid.boundary_facets
+        meas = grid.facet_measures()
+        axes, _ = facet_normal_axes(grid)
+        nv = d  # vertices per facet
+        local = (np.ones((nv, nv)) + np.eye(nv)) / (nv * (nv + 1))
+        rows, cols, vals = [], [], []
+        for a in range(nv):
+            for b in range(nv):
+                rows.append(d * facets[:, a] + axes)
+                cols.append(d * facets[:, b] + axes)
+                vals.append(meas * local[a, b])
+        n = self.space.dof_count
+        return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                             shape=(n, n)).tocsr()
+
+    def solve(self, vec):
+        rhs = -vec
+        if self.bc is not None:
+            rhs = rhs.copy()
+            rhs[self.bc] = 0.0
+        theta = self.lu.solve(rhs)
+        return theta, float(theta @ (self.form_matrix @ theta)), float(vec @ theta)
+
+
+@dataclass(frozen=True)
+class Ppl:
+    z: np.ndarray
+    lam: np.ndarray
+    mu: np.ndarray
+    delta: float = 0.5
+    r: float = 0.999
+    alpha: float = 2000.0
+    beta: float = 0.5
+
+
+def ppl_init(nc):
+    return Ppl(np.zeros(nc), np.zeros(nc), np.zeros(nc))
+
+
+def ppl_update(s, c):
+    c = np.asarray(c, dtype=float).reshape(-1)
+    gap = s.lam - s.mu
+    mu = s.mu + s.delta * gap / (float(gap @ gap) + 1.0)
+    lam = mu + s.alpha / (1.0 + s.alpha * s.beta) * (c - 1.0)
+    z = (lam - mu) / s.alpha
+    return replace(s, z=z, lam=lam, mu=mu, delta=s.r * s.delta)
+
+
+def lagrangian(cost, c, s):
+    c = np.asarray(c, dtype=float).reshape(-1)
+    gap = s.lam - s.mu
+    return float(cost + s.lam @ (c - 1.0) + s.mu @ s.z
+                 + 0.5 * s.alpha * float(s.z @ s.z) + 0.5 * s.beta * float(gap @ gap))

@@ -1,0 +1,101 @@
+// Shared device/host utilities for liblsgpu (sm_100a).
+//
+// Deterministic reductions: every reducing kernel writes one partial per CTA
+// (warp-shuffle tree + fixed-order combine of the per-warp values), and the
+// last CTA to finish (threadfence + atomic ticket) sums the partials in index
+// order.  No floating-point atomics anywhere, so results are bitwise
+// reproducible run to run -- the property the reference asserts for its
+// serial vs threaded runs (test_driver.py:183-199, test_acceptance.py:467-483).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lsgpu.h"
+
+namespace lsg {
+
+void set_error(const char *fmt, ...);
+int check_launch(const char *what);
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Reduce NV values over the CTA; slot v uses max when bit v of MAXMASK is set.
+// Result is valid in thread 0.  `scratch` holds NV * (blockDim/32) doubles.
+template <int NV, unsigned MAXMASK>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double *scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = ((MAXMASK >> i) & 1u) ? warp_max(v[i]) : warp_sum(v[i]);
+    if (lane == 0) scratch[i * nw + warp] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double acc = scratch[i * nw];
+      for (int w = 1; w < nw; ++w)
+        acc = ((MAXMASK >> i) & 1u) ? fmax(acc, scratch[i * nw + w]) : acc + scratch[i * nw + w];
+      v[i] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// Store this CTA's partial and, in the last CTA of the group, return the
+// fixed-order total of all partials in `total` (valid in thread 0 of the
+// last CTA only).  Returns true in every thread of the last CTA.
+//   partials: nblk * NV doubles for this group; counter: one uint per group.
+template <int NV, unsigned MAXMASK>
+__device__ bool block_partial_and_total(double (&v)[NV], double *partials, uint32_t *counter,
+                                        int blk, int nblk, double *scratch, double (&total)[NV]) {
+  __shared__ bool am_last;
+  block_reduce<NV, MAXMASK>(v, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) partials[(size_t)blk * NV + i] = v[i];
+    __threadfence();
+    unsigned ticket = atomicAdd(counter, 1u);
+    am_last = (ticket == (unsigned)(nblk - 1));
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  // Fixed assignment: thread t sums blocks t, t+T, ... in order; then the
+  // same fixed tree as block_reduce.
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = ((MAXMASK >> i) & 1u) ? -INFINITY : 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double x = __ldcg(partials + (size_t)b * NV + i);
+      acc[i] = ((MAXMASK >> i) & 1u) ? fmax(acc[i], x) : acc[i] + x;
+    }
+  }
+  block_reduce<NV, MAXMASK>(acc, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) total[i] = acc[i];
+    *counter = 0u;  // re-arm for the next launch
+  }
+  return true;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace lsg
