@@ -91,13 +91,19 @@ typedef struct {
 } lsg_pcg_scalars;
 
 /* PCG workspace; every pointer is device memory owned by the caller.
- *   x, b, r, p, q : k * n doubles each (n = dim * num_nodes)
+ *   x, b, r, p, q, p_alt : k * n doubles each (n = dim * num_nodes)
  *   scal          : k lsg_pcg_scalars
  *   partials      : k * lsg_partials_per_rhs() * 4 doubles
- *   counters      : k uint32, zero-initialised once by the caller */
+ *   counters      : k uint32, zero-initialised once by the caller
+ * The search direction is double-buffered (p / p_alt): the fused pass that
+ * forms p = z + beta p_old also applies the operator to it, and neighbouring
+ * CTAs read p_old in their halo, so p cannot be updated in place.  `parity`
+ * (which buffer is current) is owned by the library: lsg_pcg_start resets it,
+ * lsg_pcg_iterate flips it once per iteration; the current direction after a
+ * call is (parity ? p_alt : p). */
 typedef struct {
   int32_t k;
-  int32_t pad_;
+  int32_t parity;
   double *x;
   const double *b;
   double *r;
@@ -106,6 +112,7 @@ typedef struct {
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
+  double *p_alt;
 } lsg_pcg_ws;
 
 int32_t lsg_abi_version(void);
@@ -154,9 +161,9 @@ int lsg_diag(const lsg_op *op, double *diag, void *stream);
  * entry.  lsg_pcg_start computes r = b - A x and the stopping thresholds;
  * lsg_pcg_iterate enqueues `niter` more iterations (two fused kernels each);
  * converged right-hand sides freeze.  Poll ws->scal (done, iters). */
-int lsg_pcg_start(const lsg_op *op, const lsg_pcg_ws *ws, double rtol, double atol,
+int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol,
                   double maxiter, void *stream);
-int lsg_pcg_iterate(const lsg_op *op, const lsg_pcg_ws *ws, int32_t niter, void *stream);
+int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream);
 
 /* Fused compliance evaluation + shape-derivative right-hand side --
  * replaces ComplianceModel.cost/constraint/derivative (compliance.py:111-139,

@@ -42,10 +42,11 @@ class Op(ctypes.Structure):
 
 
 class PcgWs(ctypes.Structure):
-    _fields_ = [("k", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    _fields_ = [("k", ctypes.c_int32), ("parity", ctypes.c_int32),
                 ("x", ctypes.c_void_p), ("b", ctypes.c_void_p), ("r", ctypes.c_void_p),
                 ("p", ctypes.c_void_p), ("q", ctypes.c_void_p), ("scal", ctypes.c_void_p),
-                ("partials", ctypes.c_void_p), ("counters", ctypes.c_void_p)]
+                ("partials", ctypes.c_void_p), ("counters", ctypes.c_void_p),
+                ("p_alt", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

@@ -135,14 +135,14 @@ int lsg_diag(const lsg_op *op, double *diag_out, void *stream) {
 
 static int check_ws(const lsg_pcg_ws *ws) {
   if (!ws || ws->k < 1 || ws->k > 65535 || !ws->x || !ws->b || !ws->r || !ws->p || !ws->q ||
-      !ws->scal || !ws->partials || !ws->counters) {
+      !ws->scal || !ws->partials || !ws->counters || !ws->p_alt) {
     set_error("incomplete PCG workspace");
     return LSG_ERR_ARG;
   }
   return LSG_OK;
 }
 
-int lsg_pcg_start(const lsg_op *op, const lsg_pcg_ws *ws, double rtol, double atol, double maxiter,
+int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol, double maxiter,
                   void *stream) {
   int rc = check_op(op);
   if (!rc) rc = check_ws(ws);
@@ -151,7 +151,7 @@ int lsg_pcg_start(const lsg_op *op, const lsg_pcg_ws *ws, double rtol, double at
                   pcg_start(*op, *ws, rtol, atol, maxiter, S(stream)));
 }
 
-int lsg_pcg_iterate(const lsg_op *op, const lsg_pcg_ws *ws, int32_t niter, void *stream) {
+int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream) {
   int rc = check_op(op);
   if (!rc) rc = check_ws(ws);
   if (rc) return rc;

@@ -11,9 +11,9 @@ namespace d2 {
 int64_t partials_per_rhs(const lsg_grid &g);
 int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st);
 int diag(const lsg_op &op, double *d, cudaStream_t st);
-int pcg_start(const lsg_op &op, const lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
+int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
-int pcg_iterate(const lsg_op &op, const lsg_pcg_ws &ws, int niter, cudaStream_t st);
+int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
 int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,
@@ -36,9 +36,9 @@ namespace d3 {
 int64_t partials_per_rhs(const lsg_grid &g);
 int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st);
 int diag(const lsg_op &op, double *d, cudaStream_t st);
-int pcg_start(const lsg_op &op, const lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
+int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
-int pcg_iterate(const lsg_op &op, const lsg_pcg_ws &ws, int niter, cudaStream_t st);
+int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
 int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,

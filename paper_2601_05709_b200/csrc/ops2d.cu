@@ -745,10 +745,11 @@ int diag(const lsg_op &op, double *d, cudaStream_t st) {
   return check_launch("diag2d");
 }
 
-int pcg_start(const lsg_op &op, const lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
+int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   const int64_t n = 2 * (int64_t)(g.nx + 1) * (g.ny + 1);
+  ws.parity = 0;
   init_scalars<<<(unsigned)ceil_div(ws.k, 64), 64, 0, st>>>(ws.k, ws.scal, rtol, atol, maxiter);
   int rc = check_launch("init_scalars");
   if (rc) return rc;
@@ -766,31 +767,34 @@ int pcg_start(const lsg_op &op, const lsg_pcg_ws &ws, double rtol, double atol, 
   return check_launch("zero_if_flag");
 }
 
-int pcg_iterate(const lsg_op &op, const lsg_pcg_ws &ws, int niter, cudaStream_t st) {
+int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
   const uint8_t *w = static_cast<const uint8_t *>(op.words);
   MArgs a = {};
   a.words = op.words;
   a.x = ws.r;
-  a.x2 = ws.p;
   a.y = ws.q;
-  a.y2 = ws.p;
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
   const dim3 eg((unsigned)ceil_div(nn, kEwThreads), (unsigned)ws.k);
   for (int it = 0; it < niter; ++it) {
+    double *p_old = ws.parity ? ws.p_alt : ws.p;
+    double *p_new = ws.parity ? ws.p : ws.p_alt;
+    a.x2 = p_old;
+    a.y2 = p_new;
     int rc = dispatch_op<PCGA>(op, a, ws.k, st);
     if (rc) return rc;
     if (op.kind == LSG_OP_ELASTICITY)
-      pcg_update<Elast><<<eg, kEwThreads, 0, st>>>(make_elast(g, op), g, w, ws.x, ws.r, ws.p, ws.q,
+      pcg_update<Elast><<<eg, kEwThreads, 0, st>>>(make_elast(g, op), g, w, ws.x, ws.r, p_new, ws.q,
                                                     ws.scal, ws.partials, ws.counters);
     else
-      pcg_update<H1><<<eg, kEwThreads, 0, st>>>(make_h1(g, op), g, w, ws.x, ws.r, ws.p, ws.q,
+      pcg_update<H1><<<eg, kEwThreads, 0, st>>>(make_h1(g, op), g, w, ws.x, ws.r, p_new, ws.q,
                                                  ws.scal, ws.partials, ws.counters);
     rc = check_launch("pcg_update2d");
     if (rc) return rc;
+    ws.parity ^= 1;
   }
   return LSG_OK;
 }
