@@ -95,6 +95,7 @@ typedef struct {
  *   scal          : k lsg_pcg_scalars
  *   partials      : k * lsg_partials_per_rhs() * 4 doubles
  *   counters      : k uint32, zero-initialised once by the caller
+ *   dinv          : n doubles, lsg_inv_diag of the operator (shared by all k)
  * The search direction is double-buffered (p / p_alt): the fused pass that
  * forms p = z + beta p_old also applies the operator to it, and neighbouring
  * CTAs read p_old in their halo, so p cannot be updated in place.  `parity`
@@ -113,6 +114,7 @@ typedef struct {
   double *partials;
   uint32_t *counters;
   double *p_alt;
+  const double *dinv; /* n doubles: inverse Jacobi diagonal from lsg_inv_diag */
 } lsg_pcg_ws;
 
 int32_t lsg_abi_version(void);
@@ -154,6 +156,9 @@ int lsg_apply(const lsg_op *op, int32_t k, const double *x, double *y, void *str
 
 /* Jacobi diagonal of the eliminated operator (fem.py:303-305), n doubles. */
 int lsg_diag(const lsg_op *op, double *diag, void *stream);
+/* Its inverse as the PCG uses it: 1/d, with 1 where d == 0 (fem.py:303-305).
+ * Shared by every right-hand side of a batch; computed once per operator. */
+int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream);
 
 /* Batched Jacobi-PCG with scipy cg semantics (fem.py:294-316 via
  * scipy.sparse.linalg.cg): stop when ||r|| < max(atol, rtol*||b||), checked

@@ -46,7 +46,7 @@ class PcgWs(ctypes.Structure):
                 ("x", ctypes.c_void_p), ("b", ctypes.c_void_p), ("r", ctypes.c_void_p),
                 ("p", ctypes.c_void_p), ("q", ctypes.c_void_p), ("scal", ctypes.c_void_p),
                 ("partials", ctypes.c_void_p), ("counters", ctypes.c_void_p),
-                ("p_alt", ctypes.c_void_p)]
+                ("p_alt", ctypes.c_void_p), ("dinv", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p
@@ -71,6 +71,7 @@ SIGNATURES = {
     "lsg_h1_words": (ctypes.c_int, [_G, _P, _I, _P, _P]),
     "lsg_apply": (ctypes.c_int, [_O, _I, _P, _P, _P]),
     "lsg_diag": (ctypes.c_int, [_O, _P, _P]),
+    "lsg_inv_diag": (ctypes.c_int, [_O, _P, _P]),
     "lsg_pcg_start": (ctypes.c_int, [_O, _W, _D, _D, _D, _P]),
     "lsg_pcg_iterate": (ctypes.c_int, [_O, _W, _I, _P]),
     "lsg_shape_rhs": (ctypes.c_int, [_O, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P]),

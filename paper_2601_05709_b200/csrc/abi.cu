@@ -133,9 +133,15 @@ int lsg_diag(const lsg_op *op, double *diag_out, void *stream) {
   return DISPATCH(op->grid, diag(*op, diag_out, S(stream)), diag(*op, diag_out, S(stream)));
 }
 
+int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  return DISPATCH(op->grid, inv_diag(*op, dinv, S(stream)), inv_diag(*op, dinv, S(stream)));
+}
+
 static int check_ws(const lsg_pcg_ws *ws) {
   if (!ws || ws->k < 1 || ws->k > 65535 || !ws->x || !ws->b || !ws->r || !ws->p || !ws->q ||
-      !ws->scal || !ws->partials || !ws->counters || !ws->p_alt) {
+      !ws->scal || !ws->partials || !ws->counters || !ws->p_alt || !ws->dinv) {
     set_error("incomplete PCG workspace");
     return LSG_ERR_ARG;
   }

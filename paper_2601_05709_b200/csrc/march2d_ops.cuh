@@ -1,0 +1,367 @@
+// The 2D warp-marching kernel and its per-action epilogues (see march2d.cuh
+// for the data layout and the operator physics).
+#pragma once
+
+#include "march2d.cuh"
+
+namespace lsg {
+namespace d2 {
+
+enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4 };
+
+// Arguments shared by every marching launch (unused fields stay null).
+struct MArgs {
+  const void *words;
+  const double *x;     // APPLY/RESID/STATS: input field ; PCGA: r ; SHAPE: u (KB fields)
+  const double *x2;    // PCGA: p_old ; STATS: vec
+  const double *b;     // RESID: b
+  double *y;           // APPLY: y ; RESID: r ; PCGA: q ; SHAPE: vec_cost
+  double *y2;          // PCGA: p (written) ; SHAPE: vec_vol
+  const double *dinv;  // RESID / PCGA: inverse Jacobi diagonal (1 on Dirichlet dofs)
+  lsg_pcg_scalars *scal;
+  double *partials;
+  uint32_t *counters;
+  double *out;         // STATS / SHAPE scalar outputs
+  int seg;             // node rows per segment
+  int nstrips;
+  int accumulate;      // SHAPE: add into vec_cost / out[0] (later RHS chunks)
+};
+
+// Compliance + shape-derivative physics for KB load cases at once
+// (compliance.py:111-139, base.py:150-158, velocity.py:129-142).
+// in = KB displacement fields, out = (vec_cost[2], vec_vol[2]).
+template <int KB>
+struct Shape {
+  static constexpr int NIN = 2 * KB, NOUT = 4;
+  double lam, mu, area, inv_hx, inv_hy, inv_volume;
+  double w0, w1;  // |T| * abar(n_in) = w0 + w1 n_in
+
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 4) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t) { return 0u; }
+
+  // bulk = sum_k (2 G_k^T sigma_k - (sigma_k:eps_k) I), row-major; dens = sum_k sigma:eps.
+  __device__ __forceinline__ void tri(const double *dP, const double *dQ, double *bulk,
+                                      double &dens) const {
+    bulk[0] = bulk[1] = bulk[2] = bulk[3] = 0.0;
+    dens = 0.0;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const double Px = dP[2 * k] * inv_hx, Py = dP[2 * k + 1] * inv_hx;
+      const double Qx = dQ[2 * k] * inv_hy, Qy = dQ[2 * k + 1] * inv_hy;
+      const double exx = Px, eyy = Qy, exy = 0.5 * (Py + Qx);
+      const double tr = exx + eyy;
+      const double sxx = 2.0 * mu * exx + lam * tr, syy = 2.0 * mu * eyy + lam * tr;
+      const double sxy = 2.0 * mu * exy;
+      const double d = sxx * exx + syy * eyy + 2.0 * sxy * exy;
+      bulk[0] += 2.0 * (Px * sxx + Py * sxy) - d;  // G = [[Px, Qx], [Py, Qy]]
+      bulk[1] += 2.0 * (Px * sxy + Py * syy);
+      bulk[2] += 2.0 * (Qx * sxx + Qy * sxy);
+      bulk[3] += 2.0 * (Qx * sxy + Qy * syy) - d;
+      dens += d;
+    }
+  }
+
+  __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
+                                       const double *u11, uint32_t word, bool count, double *c00,
+                                       double *c10, double *c01, double *c11, double *part) const {
+    const bool ok = valid(word);
+    const uint32_t nl = ok ? (word & 3u) : 0u, nu = ok ? ((word >> 2) & 3u) : 0u;
+    const double wl = ok ? fma((double)nl, w1, w0) : 0.0, wu = ok ? fma((double)nu, w1, w0) : 0.0;
+    double dP[NIN], dQ[NIN], bl[4], bu[4], dl, du;
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) { dP[t] = u10[t] - u00[t]; dQ[t] = u11[t] - u10[t]; }
+    tri(dP, dQ, bl, dl);  // lower (00, 10, 11)
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) { dP[t] = u11[t] - u01[t]; dQ[t] = u01[t] - u00[t]; }
+    tri(dP, dQ, bu, du);  // upper (00, 11, 01)
+    // cost part: X = w bulk (1/hx, 0), Y = w bulk (0, 1/hy)
+    const double XLx = wl * bl[0] * inv_hx, XLy = wl * bl[2] * inv_hx;
+    const double YLx = wl * bl[1] * inv_hy, YLy = wl * bl[3] * inv_hy;
+    const double XUx = wu * bu[0] * inv_hx, XUy = wu * bu[2] * inv_hx;
+    const double YUx = wu * bu[1] * inv_hy, YUy = wu * bu[3] * inv_hy;
+    c00[0] = -XLx - YUx;  c00[1] = -XLy - YUy;
+    c10[0] = XLx - YLx;   c10[1] = XLy - YLy;
+    c11[0] = YLx + XUx;   c11[1] = YLy + XUy;
+    c01[0] = YUx - XUx;   c01[1] = YUy - XUy;
+    // volume part: |T| n_in / (3 V) * grad N
+    const double vl = area * (double)nl * (1.0 / 3.0) * inv_volume;
+    const double vu = area * (double)nu * (1.0 / 3.0) * inv_volume;
+    c00[2] = -vl * inv_hx;  c00[3] = -vu * inv_hy;
+    c10[2] = vl * inv_hx;   c10[3] = -vl * inv_hy;
+    c11[2] = vu * inv_hx;   c11[3] = vl * inv_hy;
+    c01[2] = -vu * inv_hx;  c01[3] = vu * inv_hy;
+    if (count) {
+      part[0] += wl * dl + wu * du;
+      part[1] += area * (double)(nl + nu) * (1.0 / 3.0);
+    }
+  }
+};
+
+template <class PH, int ACT>
+struct Traits {
+  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA) ? 1 : (ACT == STATS) ? 3
+                                                                     : (ACT == SHAPE) ? 2 : 0;
+  static constexpr unsigned MAXMASK = (ACT == STATS) ? 4u : 0u;
+};
+
+template <class PH>
+__device__ __forceinline__ void node_diag(const PH &ph, uint32_t w00, uint32_t wm0, uint32_t w0m,
+                                          uint32_t wmm, int i, int j, double *d);
+template <>
+__device__ __forceinline__ void node_diag<Elast>(const Elast &ph, uint32_t w00, uint32_t wm0,
+                                                 uint32_t w0m, uint32_t wmm, int, int, double *d) {
+  ph.diag(w00, wm0, w0m, wmm, d);
+}
+template <>
+__device__ __forceinline__ void node_diag<H1>(const H1 &ph, uint32_t w00, uint32_t wm0,
+                                              uint32_t w0m, uint32_t wmm, int i, int j, double *d) {
+  ph.diag(w00, wm0, w0m, wmm, i, j, d);
+}
+
+template <int ACT>
+__device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *tot) {
+  if constexpr (ACT == RESID) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    s.bb = tot[0];
+    s.rr = tot[1];
+    s.rho = tot[2];
+    const double bn = sqrt(tot[0]);
+    s.atol = fmax(s.atol, s.reserved[0] * bn);
+    s.beta = 0.0;
+    s.first = 1.0;
+    if (tot[0] == 0.0) {
+      s.zero_rhs = 1.0;
+      s.done = 1.0;
+    } else if (sqrt(tot[1]) < s.atol) {
+      s.done = 1.0;
+    }
+  } else if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    s.pq = tot[0];
+    s.alpha = s.rho / tot[0];
+  } else if constexpr (ACT == STATS) {
+    a.out[0] = tot[0];
+    a.out[1] = tot[1];
+    a.out[2] = tot[2];
+  } else if constexpr (ACT == SHAPE) {
+    if (a.accumulate) {
+      a.out[0] += tot[0];
+    } else {
+      a.out[0] = tot[0];
+      a.out[1] = tot[1];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// The marching skeleton.  PH = Elast | H1 (operators) or Shape<KB>.
+//
+// Loop structure: two node-row register sets (SA, SB) and two accumulator
+// sets alternate roles, the loop is unrolled by two so no state is copied
+// between rows, and the global loads of row r+2 are issued while row r+1 is
+// processed.  Loads are branch-free: columns outside the grid load a clamped
+// (valid) address and get material word 0, so their cells contribute nothing.
+// ----------------------------------------------------------------------------
+template <class PH, int ACT, class W>
+__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+  constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
+  constexpr int NP = Traits<PH, ACT>::NP;
+  constexpr int NPA = NP > 0 ? NP : 1;
+  constexpr int NV = (ACT == SHAPE) ? NIN / 2 : (ACT == PCGA ? 2 : 1);
+  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
+  __shared__ double scratch[NPA * kWarps];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = blockIdx.x * kWarps + warp;
+  const int rhs = blockIdx.z;
+  const W *words = static_cast<const W *>(a.words);
+  const int nx = g.nx, ny = g.ny;
+  const int64_t nxp = nx + 1;
+  const int64_t nn = nxp * (ny + 1);
+
+  double beta = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA || ACT == RESID) {
+    const lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0) return;  // uniform across the CTA
+    if constexpr (ACT == PCGA) {
+      first = s.first != 0.0;
+      beta = s.beta;
+    }
+  }
+
+  const int i = strip * kStrip - 1 + lane;
+  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
+  const bool own = node_ok && lane >= 1 && lane <= kStrip;
+  const int ic = min(max(i, 0), nx);  // clamped column: always a valid address
+  const int J0 = blockIdx.y * a.seg;
+  const int J1 = min(J0 + a.seg, ny + 1);
+  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 2;
+  const double2 *xin = reinterpret_cast<const double2 *>(a.x + voff) + ic;
+  const double2 *xin2 = reinterpret_cast<const double2 *>(ACT == PCGA ? a.x2 + voff : a.x) + ic;
+  const double2 *dvin = reinterpret_cast<const double2 *>(HAS_DINV ? a.dinv : a.x) + ic;
+  const W *win = words + ic;
+
+  double part[NPA];
+#pragma unroll
+  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
+
+  struct Raw {
+    double2 v[NV];
+    double2 dv;
+    uint32_t wc;
+  };
+  struct Row {
+    double in[NIN], rt[NIN], raw[2], dg[2];
+    uint32_t wc;
+  };
+
+  auto fetch = [&](int r, Raw &f) {
+    const int64_t off = (int64_t)r * nxp;
+    f.wc = node_ok ? (uint32_t)__ldg(win + off) : 0u;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) f.v[k] = __ldg(xin + (size_t)k * nn + off);
+    } else {
+      f.v[0] = __ldg(xin + off);
+      if constexpr (ACT == PCGA) f.v[1] = first ? make_double2(0.0, 0.0) : __ldg(xin2 + off);
+      if constexpr (HAS_DINV) f.dv = __ldg(dvin + off);
+    }
+  };
+
+  // Operator input of node row r (masked) + raw value + inverse diagonal.
+  auto prepare = [&](int r, const Raw &f, Row &S) {
+    S.wc = f.wc;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        S.in[2 * k] = f.v[k].x;
+        S.in[2 * k + 1] = f.v[k].y;
+      }
+    } else {
+      const uint32_t m = PH::mask(f.wc);
+      double2 v = f.v[0];
+      if constexpr (HAS_DINV) {
+        S.dg[0] = f.dv.x;
+        S.dg[1] = f.dv.y;
+      }
+      if constexpr (ACT == PCGA) {
+        // z = M^-1 r with M^-1 = diag(1/D) (fem.py:303-305); p = z + beta p_old
+        v = make_double2(fma(beta, f.v[1].x, v.x * f.dv.x), fma(beta, f.v[1].y, v.y * f.dv.y));
+        if (own && r >= J0 && r < J1)
+          reinterpret_cast<double2 *>(a.y2 + voff)[(int64_t)r * nxp + i] = v;
+      }
+      S.raw[0] = v.x;
+      S.raw[1] = v.y;
+      S.in[0] = (m & 1u) ? 0.0 : v.x;
+      S.in[1] = (m & 2u) ? 0.0 : v.y;
+    }
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) S.rt[t] = __shfl_down_sync(0xffffffffu, S.in[t], 1);
+  };
+
+  auto emit = [&](int r, const Row &S, const double *accv) {
+    const int64_t node = (int64_t)r * nxp + i;
+    if constexpr (ACT == SHAPE) {
+      double2 *vc = reinterpret_cast<double2 *>(a.y);
+      double2 o = make_double2(accv[0], accv[1]);
+      if (a.accumulate) {
+        const double2 old = vc[node];
+        o.x += old.x;
+        o.y += old.y;
+      } else {
+        reinterpret_cast<double2 *>(a.y2)[node] = make_double2(accv[2], accv[3]);
+      }
+      vc[node] = o;
+    } else {
+      const uint32_t m = PH::mask(S.wc);
+      const double yx = (m & 1u) ? S.raw[0] : accv[0];
+      const double yy = (m & 2u) ? S.raw[1] : accv[1];
+      if constexpr (ACT == APPLY) {
+        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(yx, yy);
+      } else if constexpr (ACT == RESID) {
+        const double2 bv = __ldg(reinterpret_cast<const double2 *>(a.b + voff) + node);
+        const double rx = bv.x - yx, ry = bv.y - yy;
+        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(rx, ry);
+        part[0] += bv.x * bv.x + bv.y * bv.y;
+        part[1] += rx * rx + ry * ry;
+        part[2] += rx * (rx * S.dg[0]) + ry * (ry * S.dg[1]);
+      } else if constexpr (ACT == PCGA) {
+        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(yx, yy);
+        part[0] += S.raw[0] * yx + S.raw[1] * yy;
+      } else if constexpr (ACT == STATS) {
+        const double2 vv = __ldg(reinterpret_cast<const double2 *>(a.x2) + node);
+        part[0] += S.raw[0] * yx + S.raw[1] * yy;
+        part[1] += vv.x * S.raw[0] + vv.y * S.raw[1];
+        part[2] = fmax(part[2], fabs(S.raw[0]) / g.hx + fabs(S.raw[1]) / g.hy);
+      }
+    }
+  };
+
+  // One row step: new row r (register set Sn, from raw f) closes cell row
+  // r-1 against the previous row Sp; emits row r-1 (accumulator ap) and
+  // starts the accumulation of row r (an).
+  auto step = [&](int r, const Raw &f, const Row &Sp, Row &Sn, double *ap, double *an) {
+    prepare(r, f, Sn);
+    double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
+    if constexpr (ACT == SHAPE) {
+      ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, own && (r - 1) >= J0, c00, c10, c01, c11, part);
+    } else {
+      ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, i, r - 1, c00, c10, c01, c11);
+    }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);
+      double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
+      if (lane == 0) up10 = up11 = 0.0;
+      ap[t] += c00[t] + up10;
+      an[t] = c01[t] + up11;
+    }
+    if (own && (r - 1) >= J0) emit(r - 1, Sp, ap);
+  };
+
+  const int jstart = max(J0 - 1, 0);
+  const int rend = min(J1, ny);
+  Row SA, SB;
+  double accA[NOUT], accB[NOUT];
+  Raw fA, fB;
+  {
+    Raw f0;
+    fetch(jstart, f0);
+    fetch(min(jstart + 1, rend), fA);
+    fetch(min(jstart + 2, rend), fB);
+    prepare(jstart, f0, SA);
+  }
+#pragma unroll
+  for (int t = 0; t < NOUT; ++t) accA[t] = 0.0;
+
+  bool last_in_b = false;  // which register set holds row rend after the loop
+  int r = jstart + 1;
+  while (r <= rend) {
+    step(r, fA, SA, SB, accA, accB);
+    fetch(min(r + 2, rend), fA);
+    if (++r > rend) { last_in_b = true; break; }
+    step(r, fB, SB, SA, accB, accA);
+    fetch(min(r + 2, rend), fB);
+    ++r;
+  }
+  if (J1 == ny + 1 && own && ny >= J0) {
+    if (last_in_b) emit(ny, SB, accB);
+    else emit(ny, SA, accA);
+  }
+
+  if constexpr (NP > 0) {
+    const int nblk = gridDim.x * gridDim.y;
+    const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+    double tot[NPA];
+    const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
+    if (block_partial_and_total<NP, Traits<PH, ACT>::MAXMASK>(part, a.partials + pbase,
+                                                              a.counters + rhs, blk, nblk,
+                                                              scratch, tot)) {
+      if (threadIdx.x == 0) finalize<ACT>(a, rhs, tot);
+    }
+  }
+}
+
+}  // namespace d2
+}  // namespace lsg

@@ -11,6 +11,7 @@ namespace d2 {
 int64_t partials_per_rhs(const lsg_grid &g);
 int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st);
 int diag(const lsg_op &op, double *d, cudaStream_t st);
+int inv_diag(const lsg_op &op, double *d, cudaStream_t st);
 int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
@@ -36,6 +37,7 @@ namespace d3 {
 int64_t partials_per_rhs(const lsg_grid &g);
 int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st);
 int diag(const lsg_op &op, double *d, cudaStream_t st);
+int inv_diag(const lsg_op &op, double *d, cudaStream_t st);
 int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);

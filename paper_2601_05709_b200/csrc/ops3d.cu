@@ -13,6 +13,7 @@ static int todo() {
 int64_t partials_per_rhs(const lsg_grid &) { return 1024; }
 int apply(const lsg_op &, int, const double *, double *, cudaStream_t) { return todo(); }
 int diag(const lsg_op &, double *, cudaStream_t) { return todo(); }
+int inv_diag(const lsg_op &, double *, cudaStream_t) { return todo(); }
 int pcg_start(const lsg_op &, lsg_pcg_ws &, double, double, double, cudaStream_t) { return todo(); }
 int pcg_iterate(const lsg_op &, lsg_pcg_ws &, int, cudaStream_t) { return todo(); }
 int shape_rhs(const lsg_op &, int, const double *, double, double *, double *, double *, double *,

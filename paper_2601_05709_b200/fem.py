@@ -173,6 +173,15 @@ class _Operator:
         _lib.call("lsg_diag", self._op(), _lib.ptr(d), _lib.stream())
         return d
 
+    def inverse_diagonal(self):
+        """Jacobi preconditioner diag(1/D) (``fem.py:303-305``), computed once per operator."""
+        dinv = getattr(self, "_dinv", None)
+        if dinv is None:
+            dinv = torch.empty(self.space.dof_count, dtype=torch.float64, device="cuda")
+            _lib.call("lsg_inv_diag", self._op(), _lib.ptr(dinv), _lib.stream())
+            self._dinv = dinv
+        return dinv
+
 
 class ElasticityOperator(_Operator):
     """Ersatz-material elasticity, Dirichlet-eliminated (``fem.py:397-411, 274-291``).
@@ -296,6 +305,8 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
     maxiter = CG_ITER_FACTOR * n if maxiter is None else int(maxiter)
     cop = op._op()
     st = _lib.stream()
+    dinv = op.inverse_diagonal()
+    ws.ws.dinv = dinv.data_ptr()
     _lib.call("lsg_pcg_start", cop, ws.ws, float(rtol), float(atol), float(maxiter), st)
     stream = torch.cuda.current_stream()
     ev = torch.cuda.Event()

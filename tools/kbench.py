@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""Kernel micro-benchmarks on the B200 (CUDA events, L2 flushed where stated).
+
+    python tools/kbench.py [--grid 1024x256] [--k 8] [--iters 200]
+
+Times the standalone elasticity apply (k RHS), and the fused PCG iteration
+(lsg_pcg_iterate with the stopping test disabled) on a random two-phase
+material, and prints per-launch times and algorithmic GB/s.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2601_05709_b200 import _lib, build_rect_mesh, build_box_mesh  # noqa: E402
+from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace, _workspace  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", default="1024x256")
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=200)
+    args = ap.parse_args()
+    n = tuple(int(v) for v in args.grid.split("x"))
+    if len(n) == 2:
+        mesh = build_rect_mesh((0.0, 0.0, 4.0, 1.0), n[0], n[1], [(1, lambda p: p[:, 1] < 1e-12)])
+        lame = (0.3 / 0.91, 1 / 2.6)
+    else:
+        mesh = build_box_mesh((0.0, 0.0, 0.0, 2.0, 1.0, 1.0), n, [(1, lambda p: p[:, 0] < 1e-12)])
+        lame = (0.576923, 0.384615)
+    d, N, E, k = mesh.dim, mesh.num_vertices, mesh.num_elements, args.k
+    space = FunctionSpace(mesh, d)
+    phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
+    op = ElasticityOperator(space, phi, lame, 1e-3, DirichletSet.on_tags(space, 1))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    out = {"grid": args.grid, "k": k, "nodes": N}
+
+    def timed(fn, reps, flush_l2):
+        ts = []
+        for rep in range(reps + 3):
+            if flush_l2:
+                flush.fill_(float(rep))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep >= 3:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        return float(np.median(ts))
+
+    u = torch.randn((k, d * N), dtype=torch.float64, device="cuda")
+    y = torch.empty_like(u)
+    cop = op._op()
+    st = _lib.stream()
+    apply = lambda: _lib.call("lsg_apply", cop, k, _lib.ptr(u), _lib.ptr(y), st)
+    for name, fl in (("apply_cold_us", True), ("apply_warm_us", False)):
+        t = timed(apply, 20, fl)
+        out[name] = t
+        out[name.replace("_us", "_frac")] = (16.0 * d * k * N + E) / (t * 1e-6) / 1e9 / peak
+    # fused PCG iterations, stopping disabled (rtol = atol = 0)
+    ws = _workspace(op, k)
+    ws.b.copy_(torch.randn((k, d * N), dtype=torch.float64, device="cuda"))
+    ws.x.zero_()
+    ws.ws.dinv = op.inverse_diagonal().data_ptr()
+    _lib.call("lsg_pcg_start", cop, ws.ws, 0.0, 0.0, 1e12, st)
+    it = args.iters
+    t = timed(lambda: _lib.call("lsg_pcg_iterate", cop, ws.ws, it, st), 3, False) / it
+    bytes_it = (80.0 * k + 16.0) * d * N + E
+    out["pcg_iter_us"] = t
+    out["pcg_gbs"] = bytes_it / (t * 1e-6) / 1e9
+    out["pcg_frac"] = out["pcg_gbs"] / peak
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
