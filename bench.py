@@ -33,7 +33,7 @@ FALLBACK_HBM = 6650.0
 # the default window (iterations 3..12), measured by this bench on B200
 # (profiles/r01_bench_notes.md); used to extrapolate the bounded CPU sample to
 # a whole iteration.  Same algorithm and stopping rule on both sides.
-CFG2_RHS_ITERS_PER_OUTER = 60000.0
+CFG2_RHS_ITERS_PER_OUTER = 127687.0
 
 
 def parse():
