@@ -1,32 +1,1187 @@
-// 3D (Kuhn tetrahedra) kernels -- placeholder until the 3D marching kernels land.
+// 3D kernels of liblsgpu: Kuhn-tetrahedron P1 operators on a structured box.
+//
+// Mesh (oracle/grid.py, mesh.cu): node (i,j,k) = (k(ny+1)+j)(nx+1)+i; cell
+// (i,j,k) holds six tetrahedra m = 0..5 following the axis permutation
+// (a,b,c) = KUHN[m] along the path P0 = v000, P1 = P0+e_a, P2 = P1+e_b,
+// P3 = v111.  With D_a = u(P1)-u(P0), D_b = u(P2)-u(P1), D_c = u(P3)-u(P2):
+//   grad N = (-e_a/h_a, e_a/h_a - e_b/h_b, e_b/h_b - e_c/h_c, e_c/h_c),
+//   du/dx_a = D_a/h_a, du/dx_b = D_b/h_b, du/dx_c = D_c/h_c,
+// so every operator reduces to three "fluxes" F_a, F_b, F_c per tet and the
+// contributions -F_a, F_a-F_b, F_b-F_c, F_c to the four path vertices.
+//
+// Execution (march3): a CTA of 8 warps covers 30 node columns (x, lanes 1..30
+// of each warp) and 8 node rows (y, one warp each; warp 0 is a halo row whose
+// outputs belong to the tile below) and marches along z.  Per plane step each
+// warp loads its row of the new plane, the neighbour row above comes through
+// shared memory, x-neighbours through shuffles; each lane evaluates the six
+// tets of cell (i, j, k) and the contributions to the eight corners are
+// combined with shuffles (x) and one shared-memory exchange (y).  Every node
+// is summed by one thread in a fixed order: deterministic, no atomics.
+//
+// Material word (uint32, lsg_material): bits 3m..3m+2 = n_in of tet m
+// (number of its 4 quadrature points with phi < 0), bit 18 = cell valid,
+// bits 19..21 = Dirichlet on ux, uy, uz of the node.
+// H1 word (lsg_h1_words): bits 4m..4m+3 = frozen flags of tet m's quadrature
+// points, bit 24 = cell valid, bit 25 = Dirichlet (all components).
+#include <math.h>
+
 #include "common.cuh"
 #include "ops.h"
 
 namespace lsg {
 namespace d3 {
 
-static int todo() {
-  set_error("3D operators are not built in this revision");
+constexpr int kStrip = 30;
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kSMs = 148;
+constexpr int kMaxPartials = 4096;
+constexpr int kEwThreads = 256;
+constexpr double kA = 0.5854101966249685, kB = 0.1381966011250105;  // 4-point rule
+
+struct Geo {
+  int nx, ny, nz;
+  double h[3], ih[3];
+};
+
+// Kuhn permutation m -> axes (a, b, c); corner bit per axis: x=1, y=2, z=4.
+__host__ __device__ constexpr int perm(int m, int s) {
+  return (m == 0) ? (s == 0 ? 0 : s == 1 ? 1 : 2)
+       : (m == 1) ? (s == 0 ? 0 : s == 1 ? 2 : 1)
+       : (m == 2) ? (s == 0 ? 1 : s == 1 ? 0 : 2)
+       : (m == 3) ? (s == 0 ? 1 : s == 1 ? 2 : 0)
+       : (m == 4) ? (s == 0 ? 2 : s == 1 ? 0 : 1)
+                  : (s == 0 ? 2 : s == 1 ? 1 : 0);
+}
+__host__ __device__ constexpr int corner(int m, int v) {  // path vertex v of tet m
+  return v == 0 ? 0 : v == 1 ? (1 << perm(m, 0)) : v == 2 ? ((1 << perm(m, 0)) | (1 << perm(m, 1))) : 7;
+}
+
+// ---------------------------------------------------------------------------
+// Physics
+// ---------------------------------------------------------------------------
+struct Elast {
+  static constexpr int NIN = 3, NOUT = 3;
+  double lam, mu, w0, w1;  // w(n) = w0 + w1 n = |T| (inside n + outside (4-n)) / 4
+  double ih[3];
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 18) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t w) { return (w >> 19) & 7u; }
+
+  template <int M>
+  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT]) const {
+    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
+    const double w = valid(word) ? fma((double)((word >> (3 * M)) & 7u), w1, w0) : 0.0;
+    double G[3][3];  // G[comp][axis] = d u_comp / d x_axis
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      G[q][a] = (u[P1][q] - u[P0][q]) * ih[a];
+      G[q][b] = (u[P2][q] - u[P1][q]) * ih[b];
+      G[q][cc] = (u[P3][q] - u[P2][q]) * ih[cc];
+    }
+    const double tr = G[0][0] + G[1][1] + G[2][2];
+    double S[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) S[p][q] = mu * (G[p][q] + G[q][p]) + (p == q ? lam * tr : 0.0);
+    double Fa[3], Fb[3], Fc[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Fa[q] = w * S[q][a] * ih[a];
+      Fb[q] = w * S[q][b] * ih[b];
+      Fc[q] = w * S[q][cc] * ih[cc];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      c[P0][q] -= Fa[q];
+      c[P1][q] += Fa[q] - Fb[q];
+      c[P2][q] += Fb[q] - Fc[q];
+      c[P3][q] += Fc[q];
+    }
+  }
+
+  __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int, int, int,
+                                       double (*c)[NOUT]) const {
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) c[v][q] = 0.0;
+    tet<0>(u, word, c); tet<1>(u, word, c); tet<2>(u, word, c);
+    tet<3>(u, word, c); tet<4>(u, word, c); tet<5>(u, word, c);
+  }
+
+  // diagonal contribution of path vertex v of tet M (component q), weight w
+  __device__ static double grad_sq(int M, int v, int q, const double *ihh, double lam_mu,
+                                   double muv) {
+    double g[3] = {0.0, 0.0, 0.0};
+    const int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    if (v == 0) g[a] = -ihh[a];
+    if (v == 1) { g[a] = ihh[a]; g[b] = -ihh[b]; }
+    if (v == 2) { g[b] = ihh[b]; g[cc] = -ihh[cc]; }
+    if (v == 3) g[cc] = ihh[cc];
+    return lam_mu * g[q] * g[q] + muv * (g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  }
+};
+
+struct H1 {
+  static constexpr int NIN = 3, NOUT = 3;
+  int nx, ny, nz;
+  double m;          // mw |T| / 20
+  double sw_t;       // sw |T|
+  double fz;         // fp |T| / 4
+  double pen[3];     // npen * facet area / 12 for faces normal to x, y, z
+  double ih[3];
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 24) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t w) { return ((w >> 25) & 1u) ? 7u : 0u; }
+
+  template <int M>
+  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT]) const {
+    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    constexpr int P[4] = {0, corner(M, 1), corner(M, 2), 7};
+    const uint32_t fq = (word >> (4 * M)) & 15u;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double Fa = sw_t * (u[P[1]][q] - u[P[0]][q]) * ih[a] * ih[a];
+      const double Fb = sw_t * (u[P[2]][q] - u[P[1]][q]) * ih[b] * ih[b];
+      const double Fc = sw_t * (u[P[3]][q] - u[P[2]][q]) * ih[cc] * ih[cc];
+      const double s = u[P[0]][q] + u[P[1]][q] + u[P[2]][q] + u[P[3]][q];
+      c[P[0]][q] += -Fa + m * (u[P[0]][q] + s);
+      c[P[1]][q] += Fa - Fb + m * (u[P[1]][q] + s);
+      c[P[2]][q] += Fb - Fc + m * (u[P[2]][q] + s);
+      c[P[3]][q] += Fc + m * (u[P[3]][q] + s);
+      if (fq) {
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          if (fq & (1u << qq)) {
+            double uq = 0.0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) uq += (v == qq ? kA : kB) * u[P[v]][q];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) c[P[v]][q] += fz * (v == qq ? kA : kB) * uq;
+          }
+        }
+      }
+    }
+  }
+
+  // boundary normal penalty: faces of the box split along the in-face
+  // diagonal through corners (0,0) and (1,1); facet mass |f|/12 (1 + delta).
+  __device__ __forceinline__ void face(int axis, int side, const double (*u)[NIN], double (*c)[NOUT]) const {
+    const int u1 = axis == 0 ? 1 : 0, v1 = axis == 2 ? 1 : 2;  // in-face axes (ascending)
+    const int base = side ? (1 << axis) : 0;
+    const int c00 = base, c10 = base | (1 << u1), c11 = base | (1 << u1) | (1 << v1),
+              c01 = base | (1 << v1);
+    const int tris[2][3] = {{c00, c10, c11}, {c00, c11, c01}};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double s = u[tris[t][0]][axis] + u[tris[t][1]][axis] + u[tris[t][2]][axis];
+#pragma unroll
+      for (int v = 0; v < 3; ++v) c[tris[t][v]][axis] += pen[axis] * (u[tris[t][v]][axis] + s);
+    }
+  }
+
+  __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int i, int j, int k,
+                                       double (*c)[NOUT]) const {
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) c[v][q] = 0.0;
+    if (!valid(word)) return;
+    tet<0>(u, word, c); tet<1>(u, word, c); tet<2>(u, word, c);
+    tet<3>(u, word, c); tet<4>(u, word, c); tet<5>(u, word, c);
+    if (pen[0] != 0.0 || pen[1] != 0.0 || pen[2] != 0.0) {
+      if (i == 0) face(0, 0, u, c);
+      if (i == nx - 1) face(0, 1, u, c);
+      if (j == 0) face(1, 0, u, c);
+      if (j == ny - 1) face(1, 1, u, c);
+      if (k == 0) face(2, 0, u, c);
+      if (k == nz - 1) face(2, 1, u, c);
+    }
+  }
+};
+
+// Fused compliance + shape-derivative RHS for KB states at once.
+template <int KB>
+struct Shape {
+  static constexpr int NIN = 3 * KB, NOUT = 6;
+  double lam, mu, vol_t, inv_volume, w0, w1;
+  double ih[3];
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 18) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t) { return 0u; }
+
+  template <int M>
+  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT],
+                                      bool count, double *part) const {
+    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
+    const bool ok = valid(word);
+    const uint32_t n = ok ? ((word >> (3 * M)) & 7u) : 0u;
+    const double w = ok ? fma((double)n, w1, w0) : 0.0;
+    double bulk[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double dens = 0.0;
+#pragma unroll
+    for (int f = 0; f < KB; ++f) {
+      double G[3][3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        G[q][a] = (u[P1][3 * f + q] - u[P0][3 * f + q]) * ih[a];
+        G[q][b] = (u[P2][3 * f + q] - u[P1][3 * f + q]) * ih[b];
+        G[q][cc] = (u[P3][3 * f + q] - u[P2][3 * f + q]) * ih[cc];
+      }
+      const double tr = G[0][0] + G[1][1] + G[2][2];
+      double S[3][3], E[3][3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          E[p][q] = 0.5 * (G[p][q] + G[q][p]);
+          S[p][q] = 2.0 * mu * E[p][q] + (p == q ? lam * tr : 0.0);
+        }
+      double d = 0.0;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) d += S[p][q] * E[p][q];
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double gts = 0.0;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) gts += G[r][p] * S[r][q];
+          bulk[p][q] += 2.0 * gts - (p == q ? d : 0.0);
+        }
+      dens += d;
+    }
+    // vec_cost: X_d = w bulk[:, d] / h_d ; vec_vol: v e_d / h_d
+    const double v = vol_t * (double)n * 0.25 * inv_volume;
+    double Xa[3], Xb[3], Xc[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Xa[q] = w * bulk[q][a] * ih[a];
+      Xb[q] = w * bulk[q][b] * ih[b];
+      Xc[q] = w * bulk[q][cc] * ih[cc];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      c[P0][q] -= Xa[q];
+      c[P1][q] += Xa[q] - Xb[q];
+      c[P2][q] += Xb[q] - Xc[q];
+      c[P3][q] += Xc[q];
+    }
+    c[P0][3 + a] -= v * ih[a];
+    c[P1][3 + a] += v * ih[a];
+    c[P1][3 + b] -= v * ih[b];
+    c[P2][3 + b] += v * ih[b];
+    c[P2][3 + cc] -= v * ih[cc];
+    c[P3][3 + cc] += v * ih[cc];
+    if (count) {
+      part[0] += w * dens;
+      part[1] += vol_t * (double)n * 0.25;
+    }
+  }
+
+  __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, bool count,
+                                       double (*c)[NOUT], double *part) const {
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) c[v][q] = 0.0;
+    tet<0>(u, word, c, count, part); tet<1>(u, word, c, count, part);
+    tet<2>(u, word, c, count, part); tet<3>(u, word, c, count, part);
+    tet<4>(u, word, c, count, part); tet<5>(u, word, c, count, part);
+  }
+};
+
+enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4 };
+
+struct MArgs {
+  const uint32_t *words;
+  const double *x, *x2, *b;
+  double *y, *y2;
+  const double *dinv;
+  lsg_pcg_scalars *scal;
+  double *partials;
+  uint32_t *counters;
+  double *out;
+  int seg, nzseg, nstrips, accumulate;
+};
+
+template <int ACT>
+struct Traits {
+  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA) ? 1 : (ACT == STATS) ? 3
+                                                                     : (ACT == SHAPE) ? 2 : 0;
+  static constexpr unsigned MAXMASK = (ACT == STATS) ? 4u : 0u;
+};
+
+template <int ACT>
+__device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *tot) {
+  if constexpr (ACT == RESID) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    s.bb = tot[0];
+    s.rr = tot[1];
+    s.rho = tot[2];
+    s.atol = fmax(s.atol, s.reserved[0] * sqrt(tot[0]));
+    s.beta = 0.0;
+    s.first = 1.0;
+    if (tot[0] == 0.0) {
+      s.zero_rhs = 1.0;
+      s.done = 1.0;
+    } else if (sqrt(tot[1]) < s.atol) {
+      s.done = 1.0;
+    }
+  } else if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    s.pq = tot[0];
+    s.alpha = s.rho / tot[0];
+  } else if constexpr (ACT == STATS) {
+    a.out[0] = tot[0];
+    a.out[1] = tot[1];
+    a.out[2] = tot[2];
+  } else if constexpr (ACT == SHAPE) {
+    if (a.accumulate) {
+      a.out[0] += tot[0];
+    } else {
+      a.out[0] = tot[0];
+      a.out[1] = tot[1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The z-marching skeleton
+// ---------------------------------------------------------------------------
+template <class PH, int ACT>
+__global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
+  constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
+  constexpr int NP = Traits<ACT>::NP;
+  constexpr int NPA = NP > 0 ? NP : 1;
+  constexpr int NF = (ACT == SHAPE) ? NIN / 3 : 1;  // fields per node load
+  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
+  __shared__ double su[kWarps + 1][NIN][32];
+  __shared__ double sc[kWarps][2 * NOUT][32];
+  __shared__ double scratch[NPA * kWarps];
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nzseg = a.nzseg;
+  const int zseg = blockIdx.z % nzseg, rhs = blockIdx.z / nzseg;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int64_t nxp = nx + 1, nyp = ny + 1;
+  const int64_t plane = nxp * nyp;
+  const int64_t nn = plane * (nz + 1);
+
+  double beta = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA || ACT == RESID) {
+    const lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0) return;  // CTA-uniform
+    if constexpr (ACT == PCGA) {
+      first = s.first != 0.0;
+      beta = s.beta;
+    }
+  }
+
+  const int i = (int)blockIdx.x * kStrip - 1 + lane;
+  const int jw = (int)blockIdx.y * (kWarps - 1) - 1 + w;  // this warp's node row
+  const int jx = jw + 1;                                  // extra row (top warp only)
+  const bool top = (w == kWarps - 1);
+  const bool col_ok = ((int)blockIdx.x < a.nstrips) && i >= 0 && i <= nx;
+  const bool row_ok = jw >= 0 && jw <= ny;
+  const bool node_ok = col_ok && row_ok;
+  const bool xrow_ok = col_ok && jx <= ny;
+  const bool own = node_ok && lane >= 1 && lane <= kStrip && w >= 1;
+  const int ic = min(max(i, 0), nx);
+  const int jc = min(max(jw, 0), ny), jxc = min(jx, ny);
+  const int K0 = zseg * a.seg;
+  const int K1 = min(K0 + a.seg, nz + 1);
+  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 3;
+  const double *xin = a.x + voff;
+  const double *xin2 = (ACT == PCGA) ? a.x2 + voff : a.x;
+
+  double part[NPA];
+#pragma unroll
+  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
+
+  // node row (j, kk) -> masked input, raw value, inverse diagonal, word
+  auto load = [&](int jj, bool ok, int kk, bool write_p, double *in, double *raw, double *dg,
+                  uint32_t &wc) {
+    const int64_t node = ((int64_t)kk * nyp + jj) * nxp + ic;
+    wc = ok ? __ldg(a.words + node) : 0u;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) in[3 * f + q] = __ldg(xin + (size_t)f * nn * 3 + node * 3 + q);
+    } else {
+      const uint32_t m = PH::mask(wc);
+      double v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = __ldg(xin + node * 3 + q);
+      if constexpr (HAS_DINV) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dg[q] = __ldg(a.dinv + node * 3 + q);
+      }
+      if constexpr (ACT == PCGA) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double po = first ? 0.0 : __ldg(xin2 + node * 3 + q);
+          v[q] = fma(beta, po, v[q] * dg[q]);
+        }
+        if (write_p) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) a.y2[voff + node * 3 + q] = v[q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        raw[q] = v[q];
+        in[q] = ((m >> q) & 1u) ? 0.0 : v[q];
+      }
+    }
+  };
+
+  auto emit = [&](int kk, uint32_t wc, const double *accv, const double *raw, const double *dg) {
+    const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double o = accv[q];
+        if (a.accumulate) o += a.y[node * 3 + q];
+        a.y[node * 3 + q] = o;
+        if (!a.accumulate) a.y2[node * 3 + q] = accv[3 + q];
+      }
+    } else {
+      const uint32_t m = PH::mask(wc);
+      double yv[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) yv[q] = ((m >> q) & 1u) ? raw[q] : accv[q];
+      if constexpr (ACT == APPLY) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.y[voff + node * 3 + q] = yv[q];
+      } else if constexpr (ACT == RESID) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double bv = __ldg(a.b + voff + node * 3 + q);
+          const double r = bv - yv[q];
+          a.y[voff + node * 3 + q] = r;
+          part[0] += bv * bv;
+          part[1] += r * r;
+          part[2] += r * (r * dg[q]);
+        }
+      } else if constexpr (ACT == PCGA) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          a.y[voff + node * 3 + q] = yv[q];
+          part[0] += raw[q] * yv[q];
+        }
+      } else if constexpr (ACT == STATS) {
+        double sp = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double vv = __ldg(a.x2 + node * 3 + q);
+          part[0] += raw[q] * yv[q];
+          part[1] += vv * raw[q];
+          sp += fabs(raw[q]) * g.ih[q];
+        }
+        part[2] = fmax(part[2], sp);
+      }
+    }
+  };
+
+  const int kstart = max(K0 - 1, 0);
+  const int kend = min(K1, nz);
+  // plane-k state of this warp's row (and of the row above, from smem)
+  double in_c[NIN], rt_c[NIN], iy_c[NIN], iyr_c[NIN], raw_c[3], dg_c[3], acc[NOUT];
+  uint32_t wc_c;
+  {
+    double in_t[NIN], raw_t[3], dg_t[3];
+    uint32_t wct;
+    load(jc, node_ok, kstart, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
+    if (top) {
+      load(jxc, xrow_ok, kstart, false, in_t, raw_t, dg_t, wct);
+#pragma unroll
+      for (int t = 0; t < NIN; ++t) su[kWarps][t][lane] = in_t[t];
+    }
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) su[w][t][lane] = in_c[t];
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      iy_c[t] = su[w + 1][t][lane];
+      rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
+      iyr_c[t] = __shfl_down_sync(0xffffffffu, iy_c[t], 1);
+    }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) acc[t] = 0.0;
+  }
+
+  for (int kk = kstart + 1; kk <= kend; ++kk) {
+    double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3];
+    uint32_t wc_n;
+    __syncthreads();  // su of the previous step fully consumed
+    load(jc, node_ok, kk, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
+    if (top) {
+      double in_t[NIN], raw_t[3], dg_t[3];
+      uint32_t wct;
+      load(jxc, xrow_ok, kk, false, in_t, raw_t, dg_t, wct);
+#pragma unroll
+      for (int t = 0; t < NIN; ++t) su[kWarps][t][lane] = in_t[t];
+    }
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) su[w][t][lane] = in_n[t];
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      iy_n[t] = su[w + 1][t][lane];
+      rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
+      iyr_n[t] = __shfl_down_sync(0xffffffffu, iy_n[t], 1);
+    }
+    // eight corners of cell (i, jw, kk-1): bit0 = +x, bit1 = +y, bit2 = +z
+    double U[8][NIN];
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      U[0][t] = in_c[t];  U[1][t] = rt_c[t];  U[2][t] = iy_c[t];  U[3][t] = iyr_c[t];
+      U[4][t] = in_n[t];  U[5][t] = rt_n[t];  U[6][t] = iy_n[t];  U[7][t] = iyr_n[t];
+    }
+    double C[8][NOUT];
+    if constexpr (ACT == SHAPE) {
+      ph.cell(U, wc_c, own && (kk - 1) >= K0, C, part);
+    } else {
+      ph.cell(U, wc_c, i, jw, kk - 1, C);
+    }
+    // x: corners with +x belong to lane+1
+    double T[4][NOUT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < NOUT; ++t) {
+        double up = __shfl_up_sync(0xffffffffu, C[2 * q + 1][t], 1);
+        if (lane == 0) up = 0.0;
+        T[q][t] = C[2 * q][t] + up;
+      }
+    // y: corners with +y (T[1]: plane k, T[3]: plane k+1) belong to warp w+1
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      sc[w][t][lane] = T[1][t];
+      sc[w][NOUT + t][lane] = T[3][t];
+    }
+    __syncthreads();
+    double nxt[NOUT];
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      const double b0 = w > 0 ? sc[w - 1][t][lane] : 0.0;
+      const double b1 = w > 0 ? sc[w - 1][NOUT + t][lane] : 0.0;
+      acc[t] += T[0][t] + b0;
+      nxt[t] = T[2][t] + b1;
+    }
+    if (own && (kk - 1) >= K0) emit(kk - 1, wc_c, acc, raw_c, dg_c);
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      in_c[t] = in_n[t]; rt_c[t] = rt_n[t]; iy_c[t] = iy_n[t]; iyr_c[t] = iyr_n[t];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { raw_c[q] = raw_n[q]; dg_c[q] = dg_n[q]; }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) acc[t] = nxt[t];
+    wc_c = wc_n;
+  }
+  if (K1 == nz + 1 && own && nz >= K0) emit(nz, wc_c, acc, raw_c, dg_c);
+
+  if constexpr (NP > 0) {
+    const int nblk = gridDim.x * gridDim.y * nzseg;
+    const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    double tot[NPA];
+    const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
+    if (block_partial_and_total<NP, Traits<ACT>::MAXMASK>(part, a.partials + pbase,
+                                                          a.counters + rhs, blk, nblk, scratch, tot)) {
+      if (threadIdx.x == 0) finalize<ACT>(a, rhs, tot);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise kernels
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kEwThreads, 4)
+    pcg_update(int64_t n, const double *dinv, double *x, double *r, const double *p,
+               const double *q, lsg_pcg_scalars *scal, double *partials, uint32_t *counters) {
+  __shared__ double scratch[2 * (kEwThreads / 32)];
+  const int rhs = blockIdx.y;
+  lsg_pcg_scalars &s = scal[rhs];
+  if (s.done != 0.0) return;
+  const double alpha = s.alpha;
+  const size_t off = (size_t)rhs * (size_t)n;
+  double part[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * kEwThreads;
+  for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
+    double P[4], Q[4], X[4], R[4], D[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + u * stride;
+      if (t < n) {
+        P[u] = __ldg(p + off + t);
+        Q[u] = __ldg(q + off + t);
+        D[u] = __ldg(dinv + t);
+        X[u] = x[off + t];
+        R[u] = r[off + t];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + u * stride;
+      if (t < n) {
+        const double xo = fma(alpha, P[u], X[u]);
+        const double ro = fma(-alpha, Q[u], R[u]);
+        x[off + t] = xo;
+        r[off + t] = ro;
+        part[0] += ro * (ro * D[u]);
+        part[1] += ro * ro;
+      }
+    }
+  }
+  double tot[2];
+  const int nblk = gridDim.x;
+  if (block_partial_and_total<2, 0u>(part, partials + (size_t)rhs * nblk * 2, counters + rhs,
+                                     blockIdx.x, nblk, scratch, tot)) {
+    if (threadIdx.x == 0) {
+      s.iters += 1.0;
+      s.rz_new = tot[0];
+      s.rr = tot[1];
+      if (sqrt(tot[1]) < s.atol) s.done = 1.0;
+      else if (s.iters >= s.maxiter) s.done = 2.0;
+      else {
+        s.beta = tot[0] / s.rho;
+        s.rho = tot[0];
+        s.first = 0.0;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cell_phi(const double *phi, int64_t n0, int64_t nxp, int64_t plane,
+                                         double *pc) {
+#pragma unroll
+  for (int cidx = 0; cidx < 8; ++cidx)
+    pc[cidx] = phi[n0 + (cidx & 1) + ((cidx >> 1) & 1) * nxp + ((cidx >> 2) & 1) * plane];
+}
+
+// chi at quadrature point q of tet m, bit-exact with oracle/fem.py phi_at_quad_sign
+__device__ __forceinline__ int tet_chi(const double *pc, int m, int q) {
+  int P[4] = {0, 0, 0, 7};
+  const int a = perm(m, 0), b = perm(m, 1);
+  P[1] = 1 << a;
+  P[2] = (1 << a) | (1 << b);
+  double v = __dmul_rn(kA, pc[P[q]]);
+  for (int o = 0; o < 4; ++o)
+    if (o != q) v = __dadd_rn(v, __dmul_rn(kB, pc[P[o]]));
+  return v < 0.0;
+}
+
+__global__ void material_kernel(Geo g, const double *phi, const uint8_t *bcmask, uint32_t *words) {
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  const int64_t nn = plane * (g.nz + 1);
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int k = (int)(node / plane);
+  const int j = (int)((node - k * plane) / nxp);
+  const int i = (int)(node - k * plane - (int64_t)j * nxp);
+  uint32_t w = ((uint32_t)(bcmask ? bcmask[node] : 0) & 7u) << 19;
+  if (i < g.nx && j < g.ny && k < g.nz) {
+    double pc[8];
+    cell_phi(phi, node, nxp, plane, pc);
+    for (int m = 0; m < 6; ++m) {
+      int n = 0;
+      for (int q = 0; q < 4; ++q) n += tet_chi(pc, m, q);
+      w |= (uint32_t)n << (3 * m);
+    }
+    w |= 1u << 18;
+  }
+  words[node] = w;
+}
+
+__global__ void indicator_kernel(Geo g, const double *phi, double *chi) {
+  const int64_t ncell = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 6 * ncell) return;
+  const int64_t c = t / 6;
+  const int m = (int)(t - c * 6);
+  const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), k = (int)(c / ((int64_t)g.nx * g.ny));
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  double pc[8];
+  cell_phi(phi, ((int64_t)k * (g.ny + 1) + j) * nxp + i, nxp, plane, pc);
+  for (int q = 0; q < 4; ++q) chi[t * 4 + q] = tet_chi(pc, m, q);
+}
+
+__global__ void h1_words_kernel(Geo g, const uint8_t *frozen_q, int zero_dirichlet, uint32_t *words) {
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  const int64_t nn = plane * (g.nz + 1);
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int k = (int)(node / plane);
+  const int j = (int)((node - k * plane) / nxp);
+  const int i = (int)(node - k * plane - (int64_t)j * nxp);
+  uint32_t w = 0;
+  if (i < g.nx && j < g.ny && k < g.nz) {
+    w |= 1u << 24;
+    if (frozen_q) {
+      const int64_t c = ((int64_t)k * g.ny + j) * g.nx + i;
+      for (int m = 0; m < 6; ++m)
+        for (int q = 0; q < 4; ++q) w |= (frozen_q[(c * 6 + m) * 4 + q] ? 1u : 0u) << (4 * m + q);
+    }
+  }
+  if (zero_dirichlet && (i == 0 || j == 0 || k == 0 || i == g.nx || j == g.ny || k == g.nz))
+    w |= 1u << 25;
+  words[node] = w;
+}
+
+// Jacobi diagonal: loop over the 8 cells x 6 tets around the node.
+template <class PH>
+__global__ void diag_kernel(PH ph, Geo g, const uint32_t *words, int kind, double p0, double p1,
+                            double *d) {
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  const int64_t nn = plane * (g.nz + 1);
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int k = (int)(node / plane);
+  const int j = (int)((node - k * plane) / nxp);
+  const int i = (int)(node - k * plane - (int64_t)j * nxp);
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int cidx = 0; cidx < 8; ++cidx) {
+    const int di = cidx & 1, dj = (cidx >> 1) & 1, dk = (cidx >> 2) & 1;
+    const int ci = i - di, cj = j - dj, ck = k - dk;  // cell whose corner cidx is this node
+    if (ci < 0 || cj < 0 || ck < 0 || ci >= g.nx || cj >= g.ny || ck >= g.nz) continue;
+    const uint32_t w = words[((int64_t)ck * (g.ny + 1) + cj) * nxp + ci];
+    if (!PH::valid(w)) continue;
+    // unit cell: the node is corner cidx; apply the cell operator to e_node
+    double U[8][3];
+    for (int q = 0; q < 3; ++q) {
+      for (int v = 0; v < 8; ++v)
+        for (int t = 0; t < 3; ++t) U[v][t] = 0.0;
+      U[cidx][q] = 1.0;
+      double C[8][3];
+      ph.cell(U, w, ci, cj, ck, C);
+      acc[q] += C[cidx][q];
+    }
+  }
+  const uint32_t m = PH::mask(words[node]);
+  for (int q = 0; q < 3; ++q) d[node * 3 + q] = ((m >> q) & 1u) ? 1.0 : acc[q];
+}
+
+__global__ void reciprocal_kernel(int64_t n, double *d) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) d[t] = fabs(d[t]) > 0.0 ? 1.0 / d[t] : 1.0;
+}
+
+__global__ void zero_if_flag(int64_t n, lsg_pcg_scalars *scal, double *x) {
+  const int rhs = blockIdx.y;
+  if (scal[rhs].zero_rhs == 0.0) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    x[(size_t)rhs * n + t] = 0.0;
+}
+
+__global__ void init_scalars(int k, lsg_pcg_scalars *scal, double rtol, double atol, double maxiter) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= k) return;
+  lsg_pcg_scalars s = {};
+  s.atol = atol;
+  s.maxiter = maxiter;
+  s.first = 1.0;
+  s.reserved[0] = rtol;
+  scal[r] = s;
+}
+
+__global__ void velocity_rhs_kernel(int64_t nn, const uint32_t *words, const double *vc,
+                                    const double *vv, double lam, double *b) {
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const bool pin = (words[node] >> 25) & 1u;
+  for (int c = 0; c < 3; ++c) {
+    const double v = vc[node * 3 + c] + lam * vv[node * 3 + c];
+    b[node * 3 + c] = pin ? 0.0 : -v;
+  }
+}
+
+// generic S0/S1 quadrature tensors -> vector, gathered over the 8 x 6 incident tets
+__global__ void tensor_rhs_kernel(Geo g, const double *s0, const double *s1, double *vec) {
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  const int64_t nn = plane * (g.nz + 1);
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= nn) return;
+  const int k = (int)(node / plane);
+  const int j = (int)((node - k * plane) / nxp);
+  const int i = (int)(node - k * plane - (int64_t)j * nxp);
+  const double wq = g.h[0] * g.h[1] * g.h[2] / 6.0 / 4.0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int cidx = 0; cidx < 8; ++cidx) {
+    const int ci = i - (cidx & 1), cj = j - ((cidx >> 1) & 1), ck = k - ((cidx >> 2) & 1);
+    if (ci < 0 || cj < 0 || ck < 0 || ci >= g.nx || cj >= g.ny || ck >= g.nz) continue;
+    const int64_t c = ((int64_t)ck * g.ny + cj) * g.nx + ci;
+    for (int m = 0; m < 6; ++m) {
+      int v = -1;
+      for (int vv = 0; vv < 4; ++vv)
+        if (corner(m, vv) == cidx) v = vv;
+      if (v < 0) continue;
+      double gr[3] = {0.0, 0.0, 0.0};
+      const int a = perm(m, 0), b = perm(m, 1), cc = perm(m, 2);
+      if (v == 0) gr[a] = -g.ih[a];
+      if (v == 1) { gr[a] = g.ih[a]; gr[b] = -g.ih[b]; }
+      if (v == 2) { gr[b] = g.ih[b]; gr[cc] = -g.ih[cc]; }
+      if (v == 3) gr[cc] = g.ih[cc];
+      const int64_t t = c * 6 + m;
+      for (int q = 0; q < 4; ++q) {
+        const double Nv = (q == v) ? kA : kB;
+        for (int comp = 0; comp < 3; ++comp) {
+          double val = 0.0;
+          if (s1) {
+            const double *S = s1 + ((t * 4 + q) * 3 + comp) * 3;
+            val += S[0] * gr[0] + S[1] * gr[1] + S[2] * gr[2];
+          }
+          if (s0) val += s0[(t * 4 + q) * 3 + comp] * Nv;
+          acc[comp] += wq * val;
+        }
+      }
+    }
+  }
+  for (int comp = 0; comp < 3; ++comp) vec[node * 3 + comp] = acc[comp];
+}
+
+// S1 of the cost per tet and quadrature point (parity path)
+__global__ void s1_kernel(Geo g, double lam, double mu, double ersatz, double inside, int k,
+                          const double *u, const double *phi, double *s1) {
+  const int64_t ncell = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 6 * ncell) return;
+  const int64_t c = t / 6;
+  const int m = (int)(t - c * 6);
+  const int i = (int)(c % g.nx), j = (int)((c / g.nx) % g.ny), kk = (int)(c / ((int64_t)g.nx * g.ny));
+  const int64_t nxp = g.nx + 1, plane = nxp * (g.ny + 1);
+  const int64_t n0 = ((int64_t)kk * (g.ny + 1) + j) * nxp + i;
+  const int64_t nn = plane * (g.nz + 1);
+  const int a = perm(m, 0), b = perm(m, 1), cc = perm(m, 2);
+  const int P[4] = {0, 1 << a, (1 << a) | (1 << b), 7};
+  auto nid = [&](int cidx) { return n0 + (cidx & 1) + ((cidx >> 1) & 1) * nxp + ((cidx >> 2) & 1) * plane; };
+  double bulk[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int f = 0; f < k; ++f) {
+    const double *U = u + (size_t)f * nn * 3;
+    double G[3][3];
+    for (int q = 0; q < 3; ++q) {
+      G[q][a] = (U[nid(P[1]) * 3 + q] - U[nid(P[0]) * 3 + q]) / g.h[a];
+      G[q][b] = (U[nid(P[2]) * 3 + q] - U[nid(P[1]) * 3 + q]) / g.h[b];
+      G[q][cc] = (U[nid(P[3]) * 3 + q] - U[nid(P[2]) * 3 + q]) / g.h[cc];
+    }
+    const double tr = G[0][0] + G[1][1] + G[2][2];
+    double S[3][3], E[3][3], d = 0.0;
+    for (int p = 0; p < 3; ++p)
+      for (int q = 0; q < 3; ++q) {
+        E[p][q] = 0.5 * (G[p][q] + G[q][p]);
+        S[p][q] = 2.0 * mu * E[p][q] + (p == q ? lam * tr : 0.0);
+      }
+    for (int p = 0; p < 3; ++p)
+      for (int q = 0; q < 3; ++q) d += S[p][q] * E[p][q];
+    for (int p = 0; p < 3; ++p)
+      for (int q = 0; q < 3; ++q) {
+        double gts = 0.0;
+        for (int r = 0; r < 3; ++r) gts += G[r][p] * S[r][q];
+        bulk[p][q] += 2.0 * gts - (p == q ? d : 0.0);
+      }
+  }
+  double pc[8];
+  cell_phi(phi, n0, nxp, plane, pc);
+  for (int q = 0; q < 4; ++q) {
+    const double A = tet_chi(pc, m, q) ? inside : ersatz;
+    for (int p = 0; p < 3; ++p)
+      for (int r = 0; r < 3; ++r) s1[((t * 4 + q) * 3 + p) * 3 + r] = A * bulk[p][r];
+  }
+}
+
+__global__ void cfl_kernel(int64_t nn, Geo g, const double *v, double *partials, uint32_t *counter,
+                           double *out) {
+  __shared__ double scratch[kEwThreads / 32];
+  double m[1] = {0.0};
+  for (int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; node < nn;
+       node += (int64_t)gridDim.x * blockDim.x)
+    m[0] = fmax(m[0], fabs(v[node * 3]) * g.ih[0] + fabs(v[node * 3 + 1]) * g.ih[1] +
+                          fabs(v[node * 3 + 2]) * g.ih[2]);
+  double tot[1];
+  if (block_partial_and_total<1, 1u>(m, partials, counter, blockIdx.x, gridDim.x, scratch, tot))
+    if (threadIdx.x == 0) out[0] = tot[0];
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static Geo geo_of(const lsg_grid &gr) {
+  Geo g;
+  g.nx = gr.n[0];
+  g.ny = gr.n[1];
+  g.nz = gr.n[2];
+  for (int a = 0; a < 3; ++a) {
+    g.h[a] = (gr.hi[a] - gr.lo[a]) / gr.n[a];
+    g.ih[a] = 1.0 / g.h[a];
+  }
+  return g;
+}
+
+static int64_t nodes_of(const Geo &g) { return (int64_t)(g.nx + 1) * (g.ny + 1) * (g.nz + 1); }
+
+static Elast make_elast(const Geo &g, const lsg_op &op) {
+  Elast e;
+  const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+  const double inside = op.p[3] > 0.0 ? op.p[3] : 1.0;
+  e.lam = op.p[0];
+  e.mu = op.p[1];
+  e.w0 = vol * op.p[2];
+  e.w1 = vol * (inside - op.p[2]) / 4.0;
+  for (int a = 0; a < 3; ++a) e.ih[a] = g.ih[a];
+  return e;
+}
+
+static H1 make_h1(const Geo &g, const lsg_op &op) {
+  H1 h;
+  const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+  h.nx = g.nx;
+  h.ny = g.ny;
+  h.nz = g.nz;
+  h.m = op.p[0] * vol / 20.0;
+  h.sw_t = op.p[1] * vol;
+  h.fz = op.p[3] * vol / 4.0;
+  const double fa[3] = {0.5 * g.h[1] * g.h[2], 0.5 * g.h[0] * g.h[2], 0.5 * g.h[0] * g.h[1]};
+  for (int a = 0; a < 3; ++a) {
+    h.pen[a] = op.p[2] * fa[a] / 12.0;
+    h.ih[a] = g.ih[a];
+  }
+  return h;
+}
+
+int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
+
+static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
+  const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
+  const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
+  const int64_t per_seg = nstrips * tiles * k;
+  const int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 2);
+  int64_t ns = slots / per_seg;
+  if (ns < 1) ns = 1;
+  int64_t s = ceil_div(g.nz + 1, ns);
+  if (s < 4) s = 4;
+  while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
+  seg = (int)s;
+  nzseg = (int)ceil_div(g.nz + 1, s);
+  grid = dim3((unsigned)nstrips, (unsigned)tiles, (unsigned)(nzseg * k));
+}
+
+template <class PH, int ACT>
+static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  static int ctas = -1;
+  if (ctas < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, march3<PH, ACT>, kThreads, 0) != cudaSuccess)
+    ctas = 2;
+  dim3 grid;
+  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid);
+  a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
+  march3<PH, ACT><<<grid, kThreads, 0, st>>>(ph, g, a);
+  return check_launch("march3d");
+}
+
+template <int ACT>
+static int dispatch(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  a.words = static_cast<const uint32_t *>(op.words);
+  if (op.kind == LSG_OP_ELASTICITY) return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_H1) return launch<H1, ACT>(make_h1(g, op), g, a, k, st);
+  set_error("unknown operator kind %d", op.kind);
   return LSG_ERR_ARG;
 }
 
-int64_t partials_per_rhs(const lsg_grid &) { return 1024; }
-int apply(const lsg_op &, int, const double *, double *, cudaStream_t) { return todo(); }
-int diag(const lsg_op &, double *, cudaStream_t) { return todo(); }
-int inv_diag(const lsg_op &, double *, cudaStream_t) { return todo(); }
-int pcg_start(const lsg_op &, lsg_pcg_ws &, double, double, double, cudaStream_t) { return todo(); }
-int pcg_iterate(const lsg_op &, lsg_pcg_ws &, int, cudaStream_t) { return todo(); }
-int shape_rhs(const lsg_op &, int, const double *, double, double *, double *, double *, double *,
-              uint32_t *, cudaStream_t) { return todo(); }
-int velocity_stats(const lsg_op &, const double *, const double *, double *, double *, uint32_t *,
-                   cudaStream_t) { return todo(); }
-int material(const lsg_grid &, const double *, const uint8_t *, void *, cudaStream_t) { return todo(); }
-int indicator(const lsg_grid &, const double *, double *, cudaStream_t) { return todo(); }
-int h1_words(const lsg_grid &, const uint8_t *, int, void *, cudaStream_t) { return todo(); }
-int velocity_rhs(const lsg_op &, const double *, const double *, double, double *, cudaStream_t) { return todo(); }
-int tensor_rhs(const lsg_grid &, const double *, const double *, double *, cudaStream_t) { return todo(); }
-int s1_tensor(const lsg_op &, int, const double *, const double *, double *, cudaStream_t) { return todo(); }
-int cfl_speed(const lsg_grid &, const double *, double *, double *, uint32_t *, cudaStream_t) { return todo(); }
+int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st) {
+  MArgs a = {};
+  a.x = x;
+  a.y = y;
+  return dispatch<APPLY>(op, a, k, st);
+}
+
+int diag(const lsg_op &op, double *d, cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  const int64_t nn = nodes_of(g);
+  const unsigned nb = (unsigned)ceil_div(nn, 128);
+  const uint32_t *w = static_cast<const uint32_t *>(op.words);
+  if (op.kind == LSG_OP_ELASTICITY)
+    diag_kernel<Elast><<<nb, 128, 0, st>>>(make_elast(g, op), g, w, op.kind, op.p[0], op.p[1], d);
+  else
+    diag_kernel<H1><<<nb, 128, 0, st>>>(make_h1(g, op), g, w, op.kind, op.p[0], op.p[1], d);
+  return check_launch("diag3d");
+}
+
+int inv_diag(const lsg_op &op, double *d, cudaStream_t st) {
+  int rc = diag(op, d, st);
+  if (rc) return rc;
+  const int64_t n = 3 * nodes_of(geo_of(op.grid));
+  reciprocal_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d);
+  return check_launch("inv_diag3d");
+}
+
+int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
+              cudaStream_t st) {
+  const int64_t n = 3 * nodes_of(geo_of(op.grid));
+  ws.parity = 0;
+  init_scalars<<<(unsigned)ceil_div(ws.k, 64), 64, 0, st>>>(ws.k, ws.scal, rtol, atol, maxiter);
+  int rc = check_launch("init_scalars3d");
+  if (rc) return rc;
+  MArgs a = {};
+  a.x = ws.x;
+  a.b = ws.b;
+  a.y = ws.r;
+  a.dinv = ws.dinv;
+  a.scal = ws.scal;
+  a.partials = ws.partials;
+  a.counters = ws.counters;
+  rc = dispatch<RESID>(op, a, ws.k, st);
+  if (rc) return rc;
+  zero_if_flag<<<dim3(64, ws.k), 256, 0, st>>>(n, ws.scal, ws.x);
+  return check_launch("zero_if_flag3d");
+}
+
+int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
+  const int64_t n = 3 * nodes_of(geo_of(op.grid));
+  MArgs a = {};
+  a.x = ws.r;
+  a.y = ws.q;
+  a.dinv = ws.dinv;
+  a.scal = ws.scal;
+  a.partials = ws.partials;
+  a.counters = ws.counters;
+  int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
+  int64_t slots = (int64_t)kSMs * 4 / ws.k;
+  if (slots < 1) slots = 1;
+  const dim3 eg((unsigned)(need < slots ? need : slots), (unsigned)ws.k);
+  for (int it = 0; it < niter; ++it) {
+    double *p_old = ws.parity ? ws.p_alt : ws.p;
+    double *p_new = ws.parity ? ws.p : ws.p_alt;
+    a.x2 = p_old;
+    a.y2 = p_new;
+    int rc = dispatch<PCGA>(op, a, ws.k, st);
+    if (rc) return rc;
+    pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.x, ws.r, p_new, ws.q, ws.scal, ws.partials,
+                                          ws.counters);
+    rc = check_launch("pcg_update3d");
+    if (rc) return rc;
+    ws.parity ^= 1;
+  }
+  return LSG_OK;
+}
+
+template <int KB>
+static int shape_chunk(const Geo &g, const lsg_op &op, const double *u, double volume, double *vc,
+                       double *vv, double *out, double *partials, uint32_t *counter, int chunk,
+                       cudaStream_t st) {
+  Shape<KB> ph;
+  const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+  const double inside = op.p[3] > 0.0 ? op.p[3] : 1.0;
+  ph.lam = op.p[0];
+  ph.mu = op.p[1];
+  ph.vol_t = vol;
+  ph.inv_volume = 1.0 / volume;
+  ph.w0 = vol * op.p[2];
+  ph.w1 = vol * (inside - op.p[2]) / 4.0;
+  for (int a = 0; a < 3; ++a) ph.ih[a] = g.ih[a];
+  MArgs a = {};
+  a.words = static_cast<const uint32_t *>(op.words);
+  a.x = u;
+  a.y = vc;
+  a.y2 = vv;
+  a.out = out;
+  a.partials = partials;
+  a.counters = counter;
+  a.accumulate = chunk > 0;
+  return launch<Shape<KB>, SHAPE>(ph, g, a, 1, st);
+}
+
+int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
+              double *out, double *partials, uint32_t *counter, cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  const int64_t nn = nodes_of(g);
+  int done = 0, chunk = 0;
+  while (done < k) {
+    const int left = k - done;
+    const double *uc = u + (size_t)done * nn * 3;
+    int rc, kb;
+    if (left >= 2) { kb = 2; rc = shape_chunk<2>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
+    else { kb = 1; rc = shape_chunk<1>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
+    if (rc) return rc;
+    done += kb;
+    ++chunk;
+  }
+  return LSG_OK;
+}
+
+int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,
+                   double *partials, uint32_t *counter, cudaStream_t st) {
+  MArgs a = {};
+  a.x = theta;
+  a.x2 = vec;
+  a.out = out;
+  a.partials = partials;
+  a.counters = counter;
+  return dispatch<STATS>(h1, a, 1, st);
+}
+
+int material(const lsg_grid &grid, const double *phi, const uint8_t *bcmask, void *words,
+             cudaStream_t st) {
+  const Geo g = geo_of(grid);
+  const int64_t nn = nodes_of(g);
+  material_kernel<<<(unsigned)ceil_div(nn, 128), 128, 0, st>>>(g, phi, bcmask,
+                                                               static_cast<uint32_t *>(words));
+  return check_launch("material3d");
+}
+
+int indicator(const lsg_grid &grid, const double *phi, double *chi, cudaStream_t st) {
+  const Geo g = geo_of(grid);
+  const int64_t nt = 6LL * g.nx * g.ny * g.nz;
+  indicator_kernel<<<(unsigned)ceil_div(nt, 128), 128, 0, st>>>(g, phi, chi);
+  return check_launch("indicator3d");
+}
+
+int h1_words(const lsg_grid &grid, const uint8_t *frozen_q, int zero_dirichlet, void *words,
+             cudaStream_t st) {
+  const Geo g = geo_of(grid);
+  const int64_t nn = nodes_of(g);
+  h1_words_kernel<<<(unsigned)ceil_div(nn, 128), 128, 0, st>>>(g, frozen_q, zero_dirichlet,
+                                                               static_cast<uint32_t *>(words));
+  return check_launch("h1_words3d");
+}
+
+int velocity_rhs(const lsg_op &h1, const double *vc, const double *vv, double lam, double *b,
+                 cudaStream_t st) {
+  const int64_t nn = nodes_of(geo_of(h1.grid));
+  velocity_rhs_kernel<<<(unsigned)ceil_div(nn, 256), 256, 0, st>>>(
+      nn, static_cast<const uint32_t *>(h1.words), vc, vv, lam, b);
+  return check_launch("velocity_rhs3d");
+}
+
+int tensor_rhs(const lsg_grid &grid, const double *s0, const double *s1, double *vec,
+               cudaStream_t st) {
+  const Geo g = geo_of(grid);
+  const int64_t nn = nodes_of(g);
+  tensor_rhs_kernel<<<(unsigned)ceil_div(nn, 128), 128, 0, st>>>(g, s0, s1, vec);
+  return check_launch("tensor_rhs3d");
+}
+
+int s1_tensor(const lsg_op &op, int k, const double *u, const double *phi, double *s1,
+              cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  const int64_t nt = 6LL * g.nx * g.ny * g.nz;
+  s1_kernel<<<(unsigned)ceil_div(nt, 128), 128, 0, st>>>(g, op.p[0], op.p[1], op.p[2],
+                                                         op.p[3] > 0.0 ? op.p[3] : 1.0, k, u, phi, s1);
+  return check_launch("s1_3d");
+}
+
+int cfl_speed(const lsg_grid &grid, const double *v, double *out, double *partials,
+              uint32_t *counter, cudaStream_t st) {
+  const Geo g = geo_of(grid);
+  cfl_kernel<<<296, kEwThreads, 0, st>>>(nodes_of(g), g, v, partials, counter, out);
+  return check_launch("cfl3d");
+}
 
 }  // namespace d3
 }  // namespace lsg
