@@ -169,6 +169,11 @@ int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream);
 int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol,
                   double maxiter, void *stream);
 int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream);
+/* The update x += alpha p of iteration i is folded into pass A of iteration
+ * i+1 (it reads p_i anyway), so a right-hand side that has just converged has
+ * one update pending: call lsg_pcg_finish once after the last lsg_pcg_iterate,
+ * before reading x. */
+int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream);
 
 /* Fused compliance evaluation + shape-derivative right-hand side --
  * replaces ComplianceModel.cost/constraint/derivative (compliance.py:111-139,

@@ -74,6 +74,7 @@ SIGNATURES = {
     "lsg_inv_diag": (ctypes.c_int, [_O, _P, _P]),
     "lsg_pcg_start": (ctypes.c_int, [_O, _W, _D, _D, _D, _P]),
     "lsg_pcg_iterate": (ctypes.c_int, [_O, _W, _I, _P]),
+    "lsg_pcg_finish": (ctypes.c_int, [_O, _W, _P]),
     "lsg_shape_rhs": (ctypes.c_int, [_O, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P]),
     "lsg_s1_tensor": (ctypes.c_int, [_O, _I, _P, _P, _P, _P]),
     "lsg_tensor_rhs": (ctypes.c_int, [_G, _P, _P, _P, _P]),

@@ -166,6 +166,13 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
                   pcg_iterate(*op, *ws, niter, S(stream)));
 }
 
+int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream) {
+  int rc = check_op(op);
+  if (!rc) rc = check_ws(ws);
+  if (rc) return rc;
+  return DISPATCH(op->grid, pcg_finish(*op, *ws, S(stream)), pcg_finish(*op, *ws, S(stream)));
+}
+
 int lsg_shape_rhs(const lsg_op *op, int32_t k, const double *u, double volume, double *vec_cost,
                   double *vec_vol, double *out, double *s1, double *partials, uint32_t *counter,
                   void *stream) {

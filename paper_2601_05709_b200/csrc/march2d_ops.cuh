@@ -18,6 +18,8 @@ struct MArgs {
   double *y;           // APPLY: y ; RESID: r ; PCGA: q ; SHAPE: vec_cost
   double *y2;          // PCGA: p (written) ; SHAPE: vec_vol
   const double *dinv;  // RESID / PCGA: inverse Jacobi diagonal (1 on Dirichlet dofs)
+  double *xs;          // PCGA: the iterate x (x += alpha_prev p_old is done here)
+  int finish_only;     // PCGA: only apply pending x updates of converged rhs
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
@@ -179,17 +181,6 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   const int64_t nxp = nx + 1;
   const int64_t nn = nxp * (ny + 1);
 
-  double beta = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA || ACT == RESID) {
-    const lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0) return;  // uniform across the CTA
-    if constexpr (ACT == PCGA) {
-      first = s.first != 0.0;
-      beta = s.beta;
-    }
-  }
-
   const int i = strip * kStrip - 1 + lane;
   const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
   const bool own = node_ok && lane >= 1 && lane <= kStrip;
@@ -197,6 +188,41 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   const int J0 = blockIdx.y * a.seg;
   const int J1 = min(J0 + a.seg, ny + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 2;
+
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0 || a.finish_only) {  // uniform across the CTA
+      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
+      // converged: apply the pending x += alpha p of its last iteration
+      const double al = s.alpha;
+      if (own) {
+        double2 *xv = reinterpret_cast<double2 *>(a.xs + voff);
+        const double2 *pv = reinterpret_cast<const double2 *>(a.x2 + voff);
+        for (int r = J0; r < J1; ++r) {
+          const int64_t node = (int64_t)r * nxp + i;
+          double2 xo = xv[node];
+          const double2 po = pv[node];
+          xo.x = fma(al, po.x, xo.x);
+          xo.y = fma(al, po.y, xo.y);
+          xv[node] = xo;
+        }
+      }
+      double d1[1] = {0.0}, t1[1];
+      const int nblk = gridDim.x * gridDim.y;
+      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk,
+                                         a.counters + rhs, blockIdx.y * gridDim.x + blockIdx.x,
+                                         nblk, scratch, t1))
+        if (threadIdx.x == 0) s.reserved[1] = 0.0;
+      return;
+    }
+    first = s.first != 0.0;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  } else if constexpr (ACT == RESID) {
+    if (a.scal[rhs].done != 0.0) return;
+  }
   const double2 *xin = reinterpret_cast<const double2 *>(a.x + voff) + ic;
   const double2 *xin2 = reinterpret_cast<const double2 *>(ACT == PCGA ? a.x2 + voff : a.x) + ic;
   const double2 *dvin = reinterpret_cast<const double2 *>(HAS_DINV ? a.dinv : a.x) + ic;
@@ -209,6 +235,7 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   struct Raw {
     double2 v[NV];
     double2 dv;
+    double2 xv;  // PCGA: x of an owned node (updated with the previous alpha)
     uint32_t wc;
   };
   struct Row {
@@ -224,7 +251,11 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
       for (int k = 0; k < NV; ++k) f.v[k] = __ldg(xin + (size_t)k * nn + off);
     } else {
       f.v[0] = __ldg(xin + off);
-      if constexpr (ACT == PCGA) f.v[1] = first ? make_double2(0.0, 0.0) : __ldg(xin2 + off);
+      if constexpr (ACT == PCGA) {
+        f.v[1] = first ? make_double2(0.0, 0.0) : __ldg(xin2 + off);
+        if (!first && own && r >= J0 && r < J1)
+          f.xv = reinterpret_cast<const double2 *>(a.xs + voff)[off + i];
+      }
       if constexpr (HAS_DINV) f.dv = __ldg(dvin + off);
     }
   };
@@ -248,8 +279,13 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
       if constexpr (ACT == PCGA) {
         // z = M^-1 r with M^-1 = diag(1/D) (fem.py:303-305); p = z + beta p_old
         v = make_double2(fma(beta, f.v[1].x, v.x * f.dv.x), fma(beta, f.v[1].y, v.y * f.dv.y));
-        if (own && r >= J0 && r < J1)
-          reinterpret_cast<double2 *>(a.y2 + voff)[(int64_t)r * nxp + i] = v;
+        if (own && r >= J0 && r < J1) {
+          const int64_t node = (int64_t)r * nxp + i;
+          reinterpret_cast<double2 *>(a.y2 + voff)[node] = v;
+          if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
+            reinterpret_cast<double2 *>(a.xs + voff)[node] =
+                make_double2(fma(alpha_prev, f.v[1].x, f.xv.x), fma(alpha_prev, f.v[1].y, f.xv.y));
+        }
       }
       S.raw[0] = v.x;
       S.raw[1] = v.y;

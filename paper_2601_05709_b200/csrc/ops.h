@@ -15,6 +15,7 @@ int inv_diag(const lsg_op &op, double *d, cudaStream_t st);
 int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
+int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
 int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,
@@ -41,6 +42,7 @@ int inv_diag(const lsg_op &op, double *d, cudaStream_t st);
 int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st);
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
+int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
 int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,

@@ -18,32 +18,28 @@ constexpr int kEwThreads = 256;
 constexpr int kUpd = 2;
 
 __global__ void __launch_bounds__(kEwThreads, 4)
-    pcg_update(int64_t nn, const double *dinv, double *x, double *r, const double *p,
-               const double *q, lsg_pcg_scalars *scal, double *partials, uint32_t *counters) {
+    pcg_update(int64_t nn, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
+               double *partials, uint32_t *counters) {
   __shared__ double scratch[2 * (kEwThreads / 32)];
   const int rhs = blockIdx.y;
   lsg_pcg_scalars &s = scal[rhs];
   if (s.done != 0.0) return;
   const double alpha = s.alpha;
   const size_t voff = (size_t)rhs * (size_t)nn * 2;
-  double2 *xv = reinterpret_cast<double2 *>(x + voff);
   double2 *rv = reinterpret_cast<double2 *>(r + voff);
-  const double2 *pv = reinterpret_cast<const double2 *>(p + voff);
   const double2 *qv = reinterpret_cast<const double2 *>(q + voff);
   const double2 *dv = reinterpret_cast<const double2 *>(dinv);
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   double part[2] = {0.0, 0.0};
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < nn;
        base += stride * kUpd) {
-    double2 P[kUpd], Q[kUpd], X[kUpd], R[kUpd], D[kUpd];
+    double2 Q[kUpd], R[kUpd], D[kUpd];
 #pragma unroll
     for (int u = 0; u < kUpd; ++u) {
       const int64_t node = base + u * stride;
       if (node < nn) {
-        P[u] = __ldg(pv + node);
         Q[u] = __ldg(qv + node);
         D[u] = __ldg(dv + node);
-        X[u] = xv[node];
         R[u] = rv[node];
       }
     }
@@ -51,12 +47,9 @@ __global__ void __launch_bounds__(kEwThreads, 4)
     for (int u = 0; u < kUpd; ++u) {
       const int64_t node = base + u * stride;
       if (node < nn) {
-        double2 xo = X[u], ro = R[u];
-        xo.x = fma(alpha, P[u].x, xo.x);
-        xo.y = fma(alpha, P[u].y, xo.y);
+        double2 ro = R[u];
         ro.x = fma(-alpha, Q[u].x, ro.x);
         ro.y = fma(-alpha, Q[u].y, ro.y);
-        xv[node] = xo;
         rv[node] = ro;
         part[0] += ro.x * (ro.x * D[u].x) + ro.y * (ro.y * D[u].y);
         part[1] += ro.x * ro.x + ro.y * ro.y;
@@ -71,6 +64,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
       s.iters += 1.0;
       s.rz_new = tot[0];
       s.rr = tot[1];
+      s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending (next pass A / finish)
       if (sqrt(tot[1]) < s.atol) {
         s.done = 1.0;
       } else if (s.iters >= s.maxiter) {
@@ -459,6 +453,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   a.partials = ws.partials;
   a.counters = ws.counters;
   a.dinv = ws.dinv;
+  a.xs = ws.x;
   const dim3 eg((unsigned)upd_blocks(nn, ws.k), (unsigned)ws.k);
   for (int it = 0; it < niter; ++it) {
     double *p_old = ws.parity ? ws.p_alt : ws.p;
@@ -467,13 +462,29 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     a.y2 = p_new;
     int rc = dispatch_op<PCGA>(op, a, ws.k, st);
     if (rc) return rc;
-    pcg_update<<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.x, ws.r, p_new, ws.q, ws.scal,
-                                          ws.partials, ws.counters);
+    pcg_update<<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
+                                          ws.counters);
     rc = check_launch("pcg_update2d");
     if (rc) return rc;
     ws.parity ^= 1;
   }
   return LSG_OK;
+}
+
+// Apply the pending x += alpha p of right-hand sides that converged in the
+// last iteration they ran (the update is otherwise folded into pass A).
+int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
+  MArgs a = {};
+  a.words = op.words;
+  a.x = ws.r;
+  a.x2 = ws.parity ? ws.p_alt : ws.p;
+  a.scal = ws.scal;
+  a.partials = ws.partials;
+  a.counters = ws.counters;
+  a.dinv = ws.dinv;
+  a.xs = ws.x;
+  a.finish_only = 1;
+  return dispatch_op<PCGA>(op, a, ws.k, st);
 }
 
 template <int KB>

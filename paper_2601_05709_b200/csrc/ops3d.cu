@@ -67,30 +67,38 @@ struct Elast {
   __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 18) & 1u; }
   __device__ __forceinline__ static uint32_t mask(uint32_t w) { return (w >> 19) & 7u; }
 
+  // Folded constants: F_d[q] = w sigma[q][d] / h_d with sigma from raw edge
+  // differences D_d = u(next path vertex) - u(this one) along axis d:
+  //   q != d: F_d[q] = w (A[d] D_d[q] + B[d][q] D_q[d]),  A[d] = mu/h_d^2, B = mu/(h_d h_q)
+  //   q == d: F_d[d] = w (2 A[d] D_d[d] + L[d] tr),        L[d] = lam/h_d, tr = sum_d D_d[d]/h_d
+  double A[3], B[3][3], L[3];
+
   template <int M>
   __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT]) const {
     constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
     constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
     const double w = valid(word) ? fma((double)((word >> (3 * M)) & 7u), w1, w0) : 0.0;
-    double G[3][3];  // G[comp][axis] = d u_comp / d x_axis
+    double D[3][3];  // D[axis][comp]
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      G[q][a] = (u[P1][q] - u[P0][q]) * ih[a];
-      G[q][b] = (u[P2][q] - u[P1][q]) * ih[b];
-      G[q][cc] = (u[P3][q] - u[P2][q]) * ih[cc];
+      D[a][q] = u[P1][q] - u[P0][q];
+      D[b][q] = u[P2][q] - u[P1][q];
+      D[cc][q] = u[P3][q] - u[P2][q];
     }
-    const double tr = G[0][0] + G[1][1] + G[2][2];
-    double S[3][3];
+    const double tr = fma(D[0][0], ih[0], fma(D[1][1], ih[1], D[2][2] * ih[2]));
+    double F[3][3];  // F[axis][comp]
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
+    for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int q = 0; q < 3; ++q) S[p][q] = mu * (G[p][q] + G[q][p]) + (p == q ? lam * tr : 0.0);
+      for (int q = 0; q < 3; ++q)
+        F[d][q] = (q == d) ? w * fma(2.0 * A[d], D[d][d], L[d] * tr)
+                           : w * fma(A[d], D[d][q], B[d][q] * D[q][d]);
     double Fa[3], Fb[3], Fc[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      Fa[q] = w * S[q][a] * ih[a];
-      Fb[q] = w * S[q][b] * ih[b];
-      Fc[q] = w * S[q][cc] * ih[cc];
+      Fa[q] = F[a][q];
+      Fb[q] = F[b][q];
+      Fc[q] = F[cc][q];
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -301,11 +309,12 @@ struct MArgs {
   const double *x, *x2, *b;
   double *y, *y2;
   const double *dinv;
+  double *xs;  // PCGA: the iterate x (x += alpha_prev p_old is done in pass A)
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
   double *out;
-  int seg, nzseg, nstrips, accumulate;
+  int seg, nzseg, nstrips, accumulate, finish_only;
 };
 
 template <int ACT>
@@ -353,7 +362,7 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 // The z-marching skeleton
 // ---------------------------------------------------------------------------
 template <class PH, int ACT>
-__global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
   constexpr int NP = Traits<ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
@@ -371,17 +380,6 @@ __global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
   const int64_t plane = nxp * nyp;
   const int64_t nn = plane * (nz + 1);
 
-  double beta = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA || ACT == RESID) {
-    const lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0) return;  // CTA-uniform
-    if constexpr (ACT == PCGA) {
-      first = s.first != 0.0;
-      beta = s.beta;
-    }
-  }
-
   const int i = (int)blockIdx.x * kStrip - 1 + lane;
   const int jw = (int)blockIdx.y * (kWarps - 1) - 1 + w;  // this warp's node row
   const int jx = jw + 1;                                  // extra row (top warp only)
@@ -396,6 +394,36 @@ __global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
   const int K0 = zseg * a.seg;
   const int K1 = min(K0 + a.seg, nz + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 3;
+
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0 || a.finish_only) {  // CTA-uniform
+      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
+      const double al = s.alpha;  // pending x += alpha p of the last iteration
+      if (own) {
+        for (int kk = K0; kk < K1; ++kk) {
+          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            a.xs[voff + node * 3 + q] = fma(al, a.x2[voff + node * 3 + q], a.xs[voff + node * 3 + q]);
+        }
+      }
+      double d1[1] = {0.0}, t1[1];
+      const int nblk = gridDim.x * gridDim.y * nzseg;
+      const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk, a.counters + rhs,
+                                         blk, nblk, scratch, t1))
+        if (threadIdx.x == 0) s.reserved[1] = 0.0;
+      return;
+    }
+    first = s.first != 0.0;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  } else if constexpr (ACT == RESID) {
+    if (a.scal[rhs].done != 0.0) return;
+  }
   const double *xin = a.x + voff;
   const double *xin2 = (ACT == PCGA) ? a.x2 + voff : a.x;
 
@@ -423,14 +451,19 @@ __global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
         for (int q = 0; q < 3; ++q) dg[q] = __ldg(a.dinv + node * 3 + q);
       }
       if constexpr (ACT == PCGA) {
+        double po[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          const double po = first ? 0.0 : __ldg(xin2 + node * 3 + q);
-          v[q] = fma(beta, po, v[q] * dg[q]);
+          po[q] = first ? 0.0 : __ldg(xin2 + node * 3 + q);
+          v[q] = fma(beta, po[q], v[q] * dg[q]);
         }
         if (write_p) {
 #pragma unroll
-          for (int q = 0; q < 3; ++q) a.y2[voff + node * 3 + q] = v[q];
+          for (int q = 0; q < 3; ++q) {
+            a.y2[voff + node * 3 + q] = v[q];
+            if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
+              a.xs[voff + node * 3 + q] = fma(alpha_prev, po[q], a.xs[voff + node * 3 + q]);
+          }
         }
       }
 #pragma unroll
@@ -604,8 +637,8 @@ __global__ void __launch_bounds__(kThreads) march3(PH ph, Geo g, MArgs a) {
 // Elementwise kernels
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kEwThreads, 4)
-    pcg_update(int64_t n, const double *dinv, double *x, double *r, const double *p,
-               const double *q, lsg_pcg_scalars *scal, double *partials, uint32_t *counters) {
+    pcg_update(int64_t n, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
+               double *partials, uint32_t *counters) {
   __shared__ double scratch[2 * (kEwThreads / 32)];
   const int rhs = blockIdx.y;
   lsg_pcg_scalars &s = scal[rhs];
@@ -615,15 +648,13 @@ __global__ void __launch_bounds__(kEwThreads, 4)
   double part[2] = {0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
-    double P[4], Q[4], X[4], R[4], D[4];
+    double Q[4], R[4], D[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t t = base + u * stride;
       if (t < n) {
-        P[u] = __ldg(p + off + t);
         Q[u] = __ldg(q + off + t);
         D[u] = __ldg(dinv + t);
-        X[u] = x[off + t];
         R[u] = r[off + t];
       }
     }
@@ -631,9 +662,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
     for (int u = 0; u < 4; ++u) {
       const int64_t t = base + u * stride;
       if (t < n) {
-        const double xo = fma(alpha, P[u], X[u]);
         const double ro = fma(-alpha, Q[u], R[u]);
-        x[off + t] = xo;
         r[off + t] = ro;
         part[0] += ro * (ro * D[u]);
         part[1] += ro * ro;
@@ -648,6 +677,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
       s.iters += 1.0;
       s.rz_new = tot[0];
       s.rr = tot[1];
+      s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending
       if (sqrt(tot[1]) < s.atol) s.done = 1.0;
       else if (s.iters >= s.maxiter) s.done = 2.0;
       else {
@@ -934,7 +964,12 @@ static Elast make_elast(const Geo &g, const lsg_op &op) {
   e.mu = op.p[1];
   e.w0 = vol * op.p[2];
   e.w1 = vol * (inside - op.p[2]) / 4.0;
-  for (int a = 0; a < 3; ++a) e.ih[a] = g.ih[a];
+  for (int a = 0; a < 3; ++a) {
+    e.ih[a] = g.ih[a];
+    e.A[a] = e.mu * g.ih[a] * g.ih[a];
+    e.L[a] = e.lam * g.ih[a];
+    for (int q = 0; q < 3; ++q) e.B[a][q] = e.mu * g.ih[a] * g.ih[q];
+  }
   return e;
 }
 
@@ -960,12 +995,15 @@ int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
   const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
   const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
+  // Short z-segments (one halo plane each): many CTAs in flight hide the
+  // per-plane latency of the serial march; at least ~4 waves when possible.
   const int64_t per_seg = nstrips * tiles * k;
   const int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  int64_t ns = slots / per_seg;
+  int64_t ns = ceil_div(4 * slots, per_seg);
   if (ns < 1) ns = 1;
   int64_t s = ceil_div(g.nz + 1, ns);
-  if (s < 4) s = 4;
+  if (s > 16) s = 16;
+  if (s < 6) s = 6;
   while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
   seg = (int)s;
   nzseg = (int)ceil_div(g.nz + 1, s);
@@ -1048,6 +1086,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   a.x = ws.r;
   a.y = ws.q;
   a.dinv = ws.dinv;
+  a.xs = ws.x;
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
@@ -1062,13 +1101,25 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     a.y2 = p_new;
     int rc = dispatch<PCGA>(op, a, ws.k, st);
     if (rc) return rc;
-    pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.x, ws.r, p_new, ws.q, ws.scal, ws.partials,
-                                          ws.counters);
+    pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
     rc = check_launch("pcg_update3d");
     if (rc) return rc;
     ws.parity ^= 1;
   }
   return LSG_OK;
+}
+
+int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
+  MArgs a = {};
+  a.x = ws.r;
+  a.x2 = ws.parity ? ws.p_alt : ws.p;
+  a.dinv = ws.dinv;
+  a.xs = ws.x;
+  a.scal = ws.scal;
+  a.partials = ws.partials;
+  a.counters = ws.counters;
+  a.finish_only = 1;
+  return dispatch<PCGA>(op, a, ws.k, st);
 }
 
 template <int KB>

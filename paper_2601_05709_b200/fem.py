@@ -332,6 +332,7 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
             prof.append(dict(kind=op.kind, k=k, n=n, events=(e0, e1), launched=int(chunk),
                              rhs_iters=float(delta.sum()), max_iters=float(delta.max())))
         chunk = min(chunk * 2, 512)
+    _lib.call("lsg_pcg_finish", cop, ws.ws, st)  # pending x += alpha p of the last iteration
     iters = _scal(ws, "iters").to(torch.int64).clone()
     failed = (done == 2).nonzero().flatten().tolist()
     x = ws.x.clone()
