@@ -14,13 +14,18 @@ from .model import Compliance, Velocity
 
 
 def build(c, velocity=True):
-    rules = [(1, c.fixed)] + [(2 + i, pred) for i, (_, pred) in enumerate(c.loads)]
+    # tag 1 = clamp; one tag per distinct load patch (first-match tagging)
+    rules, tags, seen = [(1, c.fixed)], [], {}
+    for _, pred in c.loads:
+        if id(pred) not in seen:
+            seen[id(pred)] = 2 + len(seen)
+            rules.append((seen[id(pred)], pred))
+        tags.append(seen[id(pred)])
     grid = Grid(c.lo, c.hi, c.n, rules)
     space = fem.Space(grid, grid.dim)
     clamp = fem.clamp_dofs(space, grid.facets_with_tag(1))
-    loads = []
-    for i, (g, _) in enumerate(c.loads):
-        loads.append(fem.boundary_traction_vector(space, grid.facets_with_tag(2 + i), g))
+    loads = [fem.boundary_traction_vector(space, grid.facets_with_tag(t), g)
+             for (g, _), t in zip(c.loads, tags)]
     if c.body_force is not None:
         bf = fem.body_force_vector(space, c.body_force)
         loads = [v + bf for v in loads] if loads else [bf]

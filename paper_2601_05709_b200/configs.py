@@ -85,7 +85,7 @@ def gaussian_random_field(shape, spacing, corr, seed=0):
     grids = np.meshgrid(*freqs, indexing="ij")
     k2 = sum((2.0 * math.pi * f) ** 2 for f in grids)
     spec *= np.exp(-0.5 * k2 * corr * corr)
-    out = np.fft.irfftn(spec, s=shape)
+    out = np.fft.irfftn(spec, s=shape, axes=tuple(range(len(shape))))
     out -= out.mean()
     out /= out.std()
     return out
@@ -123,8 +123,11 @@ def _cfg2(scale=1):
         niter=40)
 
 
-def _face_patch(x):
-    return lambda p: (p[:, 0] > x - 1e-12) & (np.abs(p[:, 1] - 0.5) < 0.1) & (np.abs(p[:, 2] - 0.5) < 0.1)
+def _face_patch(x, ny):
+    # |y - 0.5| < 0.1, |z - 0.5| < 0.1 (widened on coarse test grids so that the
+    # patch always contains facets)
+    half = max(0.1, 0.75 / ny)
+    return lambda p: (p[:, 0] > x - 1e-12) & (np.abs(p[:, 1] - 0.5) < half) & (np.abs(p[:, 2] - 0.5) < half)
 
 
 def _cfg3(scale=1):
@@ -132,7 +135,7 @@ def _cfg3(scale=1):
     return Case(
         name="cfg3", lo=(0.0, 0.0, 0.0), hi=(2.0, 1.0, 1.0), n=n,
         fixed=lambda p: p[:, 0] < 1e-12,
-        loads=(((0.0, -1.0, 0.0), _face_patch(2.0)),),
+        loads=(((0.0, -1.0, 0.0), _face_patch(2.0, n[1])),),
         volume_fraction=0.3,
         phi0=lambda p: -np.cos(4 * np.pi * p[:, 0]) * np.cos(4 * np.pi * p[:, 1]) * np.cos(4 * np.pi * p[:, 2]) - 0.3,
         niter=30)
@@ -154,10 +157,11 @@ def _cfg4(scale=1):
 def _cfg5(scale=1):
     n = (192 // scale, 96 // scale, 96 // scale)
     dirs = ((0.0, -1.0, 0.0), (0.0, 0.0, -1.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0))
+    patch = _face_patch(2.0, n[1])  # one patch (one facet tag) shared by the 4 load cases
     return Case(
         name="cfg5", lo=(0.0, 0.0, 0.0), hi=(2.0, 1.0, 1.0), n=n,
         fixed=lambda p: p[:, 0] < 1e-12,
-        loads=tuple((d, _face_patch(2.0)) for d in dirs),
+        loads=tuple((d, patch) for d in dirs),
         volume_fraction=0.25,
         phi0=lambda p: -np.cos(6 * np.pi * p[:, 0]) * np.cos(6 * np.pi * p[:, 1]) * np.cos(6 * np.pi * p[:, 2]) - 0.3,
         niter=20)
@@ -170,13 +174,26 @@ def case(name, scale=1):
     return CASES[name](scale)
 
 
+def load_tag_rules(c):
+    """Boundary tag rules (tag 1 = clamp, then one tag per distinct load patch)
+    and the tag of each load case; load cases sharing a patch predicate share
+    its tag, since tagging is first-match-wins (mesh.py:182-198)."""
+    rules, tags, seen = [(1, c.fixed)], [], {}
+    for _, pred in c.loads:
+        if id(pred) not in seen:
+            seen[id(pred)] = 2 + len(seen)
+            rules.append((seen[id(pred)], pred))
+        tags.append(seen[id(pred)])
+    return rules, tags
+
+
 def build(c, device_phi=True):
     """Product-side model, initial level set and RunParams for a Case."""
     from . import (ComplianceModel, CompliancePlusModel, FemField, FunctionSpace, LevelSetField,
                    RunParams, build_box_mesh, build_rect_mesh)
     from .velocity import BilinearSpec
 
-    rules = [(1, c.fixed)] + [(2 + i, pred) for i, (_, pred) in enumerate(c.loads)]
+    rules, load_tags = load_tag_rules(c)
     if c.dim == 2:
         mesh = build_rect_mesh((c.lo[0], c.lo[1], c.hi[0], c.hi[1]), c.n[0], c.n[1], rules)
     else:
@@ -184,10 +201,10 @@ def build(c, device_phi=True):
     bil = BilinearSpec(mass_weight=c.h1[0], stiffness_weight=c.h1[1])
     kw = dict(lame=c.lame, bilinear=bil, ersatz=c.ersatz)
     if len(c.loads) > 1:
-        model = CompliancePlusModel(mesh, 1, [(g, 2 + i) for i, (g, _) in enumerate(c.loads)],
+        model = CompliancePlusModel(mesh, 1, [(g, t) for (g, _), t in zip(c.loads, load_tags)],
                                     c.volume, **kw)
     elif len(c.loads) == 1:
-        model = ComplianceModel(mesh, 1, 2, c.loads[0][0], c.volume, **kw)
+        model = ComplianceModel(mesh, 1, load_tags[0], c.loads[0][0], c.volume, **kw)
     else:
         model = ComplianceModel(mesh, 1, None, None, c.volume, body_force=c.body_force, **kw)
     phi_vals = c.phi0(mesh.vertices if c.name != "cfg4" else None)
