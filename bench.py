@@ -48,6 +48,15 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic():
+    """DRAM bytes per fused PCG iteration from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_pcg.json")) as f:
+            return float(json.load(f)["traffic_bytes_per_pcg_iteration"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -324,7 +333,12 @@ def b200_arm(args, world, rank, local):
                                                    "elasticity apply + p.q ; pass B: x/r update + "
                                                    "Jacobi + r.z, r.r)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(),
+                         "traffic_note": "DRAM bytes per PCG iteration (pass A + pass B) from "
+                                         "profiles/r01_ncu_pcg.json; below the algorithmic count "
+                                         "because x += alpha p is folded into pass A (9 of the "
+                                         "canonical 10 vectors) and some writes stay in L2",
+                         "peak_kind": peak_kind,
                          "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration",
                          "pcg_ms_in_timed_region": pcg_ms, "pcg_share_of_step": all_ms / (t_local * 1e3),
                          "rhs_iterations": rhs_iters, "launched_iterations": launched_iters},
