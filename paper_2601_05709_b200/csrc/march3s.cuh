@@ -1,0 +1,340 @@
+// 3D z-marching kernel with an asynchronous shared-memory staging pipeline.
+//
+// Same decomposition as described in ops3d.cu (CTA = 8 warps = 8 node rows
+// incl. one halo row, 30 owned columns per warp, marching along z), but the
+// global loads of planes k+1 and k+2 are in flight as cp.async (LDGSTS)
+// copies into a 3-slot ring while plane k is computed: no registers are spent
+// on prefetching and no warp waits on a load it issued in the same step.  The
+// row above (y+1) is read from the staged plane and its operator input is
+// recomputed locally (3 FMAs per node), so the only cross-warp exchange left
+// is the y-contribution hand-off: two barriers per plane.
+#pragma once
+
+namespace lsg {
+namespace d3 {
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// doubles staged per node: APPLY/STATS: input (3); RESID: x, dinv (6);
+// PCGA: r, p_old, dinv, x (12); SHAPE: KB states (3 KB)
+template <class PH, int ACT>
+struct Stage {
+  static constexpr int NR = (ACT == PCGA) ? 12 : (ACT == RESID) ? 6 : PH::NIN;
+  static constexpr int NOUT = PH::NOUT;
+  static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NR * 32;
+  static constexpr size_t words = (size_t)3 * (kWarps + 1) * 32;
+  static constexpr size_t xchg = (size_t)kWarps * 2 * NOUT * 32;
+  static constexpr size_t bytes = doubles * 8 + xchg * 8 + words * 4;
+};
+
+template <class PH, int ACT>
+__global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
+  constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
+  constexpr int NP = Traits<ACT>::NP;
+  constexpr int NPA = NP > 0 ? NP : 1;
+  constexpr int NR = Stage<PH, ACT>::NR;
+  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *stage = reinterpret_cast<double *>(smem_raw);               // [3][kWarps+1][NR][32]
+  double *xchg = stage + Stage<PH, ACT>::doubles;                      // [kWarps][2*NOUT][32]
+  uint32_t *stw = reinterpret_cast<uint32_t *>(xchg + Stage<PH, ACT>::xchg);  // [3][kWarps+1][32]
+  __shared__ double scratch[NPA * kWarps];
+  auto ST = [&](int slot, int row, int t, int l) -> double & {
+    return stage[(((size_t)slot * (kWarps + 1) + row) * NR + t) * 32 + l];
+  };
+  auto SW = [&](int slot, int row, int l) -> uint32_t & {
+    return stw[((size_t)slot * (kWarps + 1) + row) * 32 + l];
+  };
+  auto SC = [&](int wr, int t, int l) -> double & { return xchg[((size_t)wr * 2 * NOUT + t) * 32 + l]; };
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nzseg = a.nzseg;
+  const int zseg = blockIdx.z % nzseg, rhs = blockIdx.z / nzseg;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int64_t nxp = nx + 1, nyp = ny + 1;
+  const int64_t plane = nxp * nyp;
+  const int64_t nn = plane * (nz + 1);
+
+  const int i = (int)blockIdx.x * kStrip - 1 + lane;
+  const int jw = (int)blockIdx.y * (kWarps - 1) - 1 + w;
+  const int jx = jw + 1;
+  const bool top = (w == kWarps - 1);
+  const bool col_ok = ((int)blockIdx.x < a.nstrips) && i >= 0 && i <= nx;
+  const bool node_ok = col_ok && jw >= 0 && jw <= ny;
+  const bool up_ok = col_ok && jx >= 0 && jx <= ny;  // the row above exists
+  const bool own = node_ok && lane >= 1 && lane <= kStrip && w >= 1;
+  const int ic = min(max(i, 0), nx);
+  const int jc = min(max(jw, 0), ny), jxc = min(max(jx, 0), ny);
+  const int K0 = zseg * a.seg;
+  const int K1 = min(K0 + a.seg, nz + 1);
+  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 3;
+
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0 || a.finish_only) {  // CTA-uniform
+      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
+      const double al = s.alpha;  // pending x += alpha p of the last iteration
+      if (own) {
+        for (int kk = K0; kk < K1; ++kk) {
+          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            a.xs[voff + node * 3 + q] = fma(al, a.x2[voff + node * 3 + q], a.xs[voff + node * 3 + q]);
+        }
+      }
+      double d1[1] = {0.0}, t1[1];
+      const int nblk = gridDim.x * gridDim.y * nzseg;
+      const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk, a.counters + rhs,
+                                         blk, nblk, scratch, t1))
+        if (threadIdx.x == 0) s.reserved[1] = 0.0;
+      return;
+    }
+    first = s.first != 0.0;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  } else if constexpr (ACT == RESID) {
+    if (a.scal[rhs].done != 0.0) return;
+  }
+
+  double part[NPA];
+#pragma unroll
+  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
+
+  const int kstart = max(K0 - 1, 0);
+  const int kend = min(K1, nz);
+
+  // stage plane kk of this warp's row (and, for the top warp, of the row above)
+  auto issue = [&](int kk, int slot) {
+    if (kk <= kend) {
+      const int nrows = top ? 2 : 1;
+      for (int rr = 0; rr < nrows; ++rr) {
+        const int row = rr == 0 ? jc : jxc;
+        const int srow = w + rr;
+        const int64_t node = ((int64_t)kk * nyp + row) * nxp + ic;
+        cp_async4(&SW(slot, srow, lane), a.words + node);
+        const double *src[4];
+        int ns;
+        if constexpr (ACT == PCGA) {
+          src[0] = a.x + voff; src[1] = a.x2 + voff; src[2] = a.dinv; src[3] = a.xs + voff; ns = 4;
+        } else if constexpr (ACT == RESID) {
+          src[0] = a.x + voff; src[1] = a.dinv; ns = 2;
+        } else if constexpr (ACT == SHAPE) {
+          for (int f = 0; f < NIN / 3; ++f) src[f] = a.x + (size_t)f * nn * 3;
+          ns = NIN / 3;
+        } else {
+          src[0] = a.x + voff; ns = 1;
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (s < ns) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) cp_async8(&ST(slot, srow, 3 * s + q, lane), src[s] + node * 3 + q);
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  // operator input (masked), raw value, inverse diagonal of a staged row
+  auto prepare = [&](int kk, int slot, int srow, bool ok, bool write_own, double *in, double *raw,
+                     double *dg, uint32_t &wc) {
+    wc = ok ? SW(slot, srow, lane) : 0u;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int t = 0; t < NIN; ++t) in[t] = ST(slot, srow, t, lane);
+    } else {
+      const uint32_t m = PH::mask(wc);
+      double v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = ST(slot, srow, q, lane);
+      if constexpr (ACT == RESID) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dg[q] = ST(slot, srow, 3 + q, lane);
+      }
+      if constexpr (ACT == PCGA) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          dg[q] = ST(slot, srow, 6 + q, lane);
+          const double po = first ? 0.0 : ST(slot, srow, 3 + q, lane);
+          v[q] = fma(beta, po, v[q] * dg[q]);
+        }
+        if (write_own) {
+          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            a.y2[voff + node * 3 + q] = v[q];
+            if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
+              a.xs[voff + node * 3 + q] =
+                  fma(alpha_prev, ST(slot, srow, 3 + q, lane), ST(slot, srow, 9 + q, lane));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        raw[q] = v[q];
+        in[q] = ((m >> q) & 1u) ? 0.0 : v[q];
+      }
+    }
+  };
+
+  auto emit = [&](int kk, uint32_t wc, const double *accv, const double *raw, const double *dg) {
+    const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+    if constexpr (ACT == SHAPE) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double o = accv[q];
+        if (a.accumulate) o += a.y[node * 3 + q];
+        a.y[node * 3 + q] = o;
+        if (!a.accumulate) a.y2[node * 3 + q] = accv[3 + q];
+      }
+    } else {
+      const uint32_t m = PH::mask(wc);
+      double yv[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) yv[q] = ((m >> q) & 1u) ? raw[q] : accv[q];
+      if constexpr (ACT == APPLY) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.y[voff + node * 3 + q] = yv[q];
+      } else if constexpr (ACT == RESID) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double bv = __ldg(a.b + voff + node * 3 + q);
+          const double r = bv - yv[q];
+          a.y[voff + node * 3 + q] = r;
+          part[0] += bv * bv;
+          part[1] += r * r;
+          part[2] += r * (r * dg[q]);
+        }
+      } else if constexpr (ACT == PCGA) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          a.y[voff + node * 3 + q] = yv[q];
+          part[0] += raw[q] * yv[q];
+        }
+      } else if constexpr (ACT == STATS) {
+        double sp = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double vv = __ldg(a.x2 + node * 3 + q);
+          part[0] += raw[q] * yv[q];
+          part[1] += vv * raw[q];
+          sp += fabs(raw[q]) * g.ih[q];
+        }
+        part[2] = fmax(part[2], sp);
+      }
+    }
+  };
+
+  double in_c[NIN], rt_c[NIN], iy_c[NIN], iyr_c[NIN], raw_c[3], dg_c[3], acc[NOUT];
+  uint32_t wc_c;
+  issue(kstart, kstart % 3);
+  issue(kstart + 1, (kstart + 1) % 3);
+  {
+    cp_async_wait<1>();
+    __syncthreads();
+    issue(kstart + 2, (kstart + 2) % 3);
+    double raw_t[3], dg_t[3];
+    uint32_t wt;
+    const int s0 = kstart % 3;
+    prepare(kstart, s0, w, node_ok, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
+    prepare(kstart, s0, w + 1, up_ok, false, iy_c, raw_t, dg_t, wt);
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
+      iyr_c[t] = __shfl_down_sync(0xffffffffu, iy_c[t], 1);
+    }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) acc[t] = 0.0;
+  }
+
+  for (int kk = kstart + 1; kk <= kend; ++kk) {
+    cp_async_wait<1>();  // plane kk has landed (kk+1 may still be in flight)
+    __syncthreads();     // ... for every thread; slot (kk-1)%3 is no longer read
+    issue(kk + 2, (kk + 2) % 3);
+    const int sl = kk % 3;
+    double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3], raw_t[3], dg_t[3];
+    uint32_t wc_n, wt;
+    prepare(kk, sl, w, node_ok, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
+    prepare(kk, sl, w + 1, up_ok, false, iy_n, raw_t, dg_t, wt);
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
+      iyr_n[t] = __shfl_down_sync(0xffffffffu, iy_n[t], 1);
+    }
+    double U[8][NIN];
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      U[0][t] = in_c[t];  U[1][t] = rt_c[t];  U[2][t] = iy_c[t];  U[3][t] = iyr_c[t];
+      U[4][t] = in_n[t];  U[5][t] = rt_n[t];  U[6][t] = iy_n[t];  U[7][t] = iyr_n[t];
+    }
+    double C[8][NOUT];
+    if constexpr (ACT == SHAPE) {
+      ph.cell(U, wc_c, own && (kk - 1) >= K0, C, part);
+    } else {
+      ph.cell(U, wc_c, i, jw, kk - 1, C);
+    }
+    double T[4][NOUT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < NOUT; ++t) {
+        double up = __shfl_up_sync(0xffffffffu, C[2 * q + 1][t], 1);
+        if (lane == 0) up = 0.0;
+        T[q][t] = C[2 * q][t] + up;
+      }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      SC(w, t, lane) = T[1][t];
+      SC(w, NOUT + t, lane) = T[3][t];
+    }
+    __syncthreads();
+    double nxt[NOUT];
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      const double b0 = w > 0 ? SC(w - 1, t, lane) : 0.0;
+      const double b1 = w > 0 ? SC(w - 1, NOUT + t, lane) : 0.0;
+      acc[t] += T[0][t] + b0;
+      nxt[t] = T[2][t] + b1;
+    }
+    if (own && (kk - 1) >= K0) emit(kk - 1, wc_c, acc, raw_c, dg_c);
+#pragma unroll
+    for (int t = 0; t < NIN; ++t) {
+      in_c[t] = in_n[t]; rt_c[t] = rt_n[t]; iy_c[t] = iy_n[t]; iyr_c[t] = iyr_n[t];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { raw_c[q] = raw_n[q]; dg_c[q] = dg_n[q]; }
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) acc[t] = nxt[t];
+    wc_c = wc_n;
+  }
+  cp_async_wait<0>();
+  if (K1 == nz + 1 && own && nz >= K0) emit(nz, wc_c, acc, raw_c, dg_c);
+
+  if constexpr (NP > 0) {
+    const int nblk = gridDim.x * gridDim.y * nzseg;
+    const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    double tot[NPA];
+    const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
+    if (block_partial_and_total<NP, Traits<ACT>::MAXMASK>(part, a.partials + pbase,
+                                                          a.counters + rhs, blk, nblk, scratch, tot)) {
+      if (threadIdx.x == 0) finalize<ACT>(a, rhs, tot);
+    }
+  }
+}
+
+}  // namespace d3
+}  // namespace lsg

@@ -86,26 +86,20 @@ struct Elast {
       D[cc][q] = u[P3][q] - u[P2][q];
     }
     const double tr = fma(D[0][0], ih[0], fma(D[1][1], ih[1], D[2][2] * ih[2]));
-    double F[3][3];  // F[axis][comp]
+    double T[3][3];  // unweighted fluxes T[axis][comp] = sigma[comp][axis] / h_axis
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        F[d][q] = (q == d) ? w * fma(2.0 * A[d], D[d][d], L[d] * tr)
-                           : w * fma(A[d], D[d][q], B[d][q] * D[q][d]);
-    double Fa[3], Fb[3], Fc[3];
+        T[d][q] = (q == d) ? fma(2.0 * A[d], D[d][d], L[d] * tr)
+                           : fma(A[d], D[d][q], B[d][q] * D[q][d]);
+    // weighted contributions -wT_a, w(T_a - T_b), w(T_b - T_c), wT_c via FMA
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      Fa[q] = F[a][q];
-      Fb[q] = F[b][q];
-      Fc[q] = F[cc][q];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      c[P0][q] -= Fa[q];
-      c[P1][q] += Fa[q] - Fb[q];
-      c[P2][q] += Fb[q] - Fc[q];
-      c[P3][q] += Fc[q];
+      c[P0][q] = fma(-w, T[a][q], c[P0][q]);
+      c[P1][q] = fma(w, T[a][q] - T[b][q], c[P1][q]);
+      c[P2][q] = fma(w, T[b][q] - T[cc][q], c[P2][q]);
+      c[P3][q] = fma(w, T[cc][q], c[P3][q]);
     }
   }
 
@@ -368,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
   constexpr int NPA = NP > 0 ? NP : 1;
   constexpr int NF = (ACT == SHAPE) ? NIN / 3 : 1;  // fields per node load
   constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
-  __shared__ double su[kWarps + 1][NIN][32];
+  __shared__ double su[2][kWarps + 1][NIN][32];  // double-buffered by plane parity
   __shared__ double sc[kWarps][2 * NOUT][32];
   __shared__ double scratch[NPA * kWarps];
 
@@ -534,14 +528,14 @@ __global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
     if (top) {
       load(jxc, xrow_ok, kstart, false, in_t, raw_t, dg_t, wct);
 #pragma unroll
-      for (int t = 0; t < NIN; ++t) su[kWarps][t][lane] = in_t[t];
+      for (int t = 0; t < NIN; ++t) su[kstart & 1][kWarps][t][lane] = in_t[t];
     }
 #pragma unroll
-    for (int t = 0; t < NIN; ++t) su[w][t][lane] = in_c[t];
+    for (int t = 0; t < NIN; ++t) su[kstart & 1][w][t][lane] = in_c[t];
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
-      iy_c[t] = su[w + 1][t][lane];
+      iy_c[t] = su[kstart & 1][w + 1][t][lane];
       rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
       iyr_c[t] = __shfl_down_sync(0xffffffffu, iy_c[t], 1);
     }
@@ -552,21 +546,21 @@ __global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
   for (int kk = kstart + 1; kk <= kend; ++kk) {
     double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3];
     uint32_t wc_n;
-    __syncthreads();  // su of the previous step fully consumed
+    // (no barrier needed here: su is double-buffered by plane parity)
     load(jc, node_ok, kk, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
     if (top) {
       double in_t[NIN], raw_t[3], dg_t[3];
       uint32_t wct;
       load(jxc, xrow_ok, kk, false, in_t, raw_t, dg_t, wct);
 #pragma unroll
-      for (int t = 0; t < NIN; ++t) su[kWarps][t][lane] = in_t[t];
+      for (int t = 0; t < NIN; ++t) su[kk & 1][kWarps][t][lane] = in_t[t];
     }
 #pragma unroll
-    for (int t = 0; t < NIN; ++t) su[w][t][lane] = in_n[t];
+    for (int t = 0; t < NIN; ++t) su[kk & 1][w][t][lane] = in_n[t];
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
-      iy_n[t] = su[w + 1][t][lane];
+      iy_n[t] = su[kk & 1][w + 1][t][lane];
       rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
       iyr_n[t] = __shfl_down_sync(0xffffffffu, iy_n[t], 1);
     }
@@ -632,6 +626,14 @@ __global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
     }
   }
 }
+
+}  // namespace d3
+}  // namespace lsg
+
+#include "march3s.cuh"
+
+namespace lsg {
+namespace d3 {
 
 // ---------------------------------------------------------------------------
 // Elementwise kernels
@@ -1013,12 +1015,17 @@ static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int 
 template <class PH, int ACT>
 static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   static int ctas = -1;
-  if (ctas < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, march3<PH, ACT>, kThreads, 0) != cudaSuccess)
-    ctas = 2;
+  constexpr size_t smem = Stage<PH, ACT>::bytes;
+  if (ctas < 0) {
+    cudaFuncSetAttribute(march3s<PH, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, march3s<PH, ACT>, kThreads, smem) !=
+        cudaSuccess)
+      ctas = 2;
+  }
   dim3 grid;
   launch_geometry(g, k, ctas, a.seg, a.nzseg, grid);
   a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
-  march3<PH, ACT><<<grid, kThreads, 0, st>>>(ph, g, a);
+  march3s<PH, ACT><<<grid, kThreads, smem, st>>>(ph, g, a);
   return check_launch("march3d");
 }
 
@@ -1157,8 +1164,9 @@ int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *v
     const int left = k - done;
     const double *uc = u + (size_t)done * nn * 3;
     int rc, kb;
-    if (left >= 2) { kb = 2; rc = shape_chunk<2>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
-    else { kb = 1; rc = shape_chunk<1>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
+    (void)left;  // one state per launch in 3D (static shared memory of the 2-state variant > 48 KB)
+    kb = 1;
+    rc = shape_chunk<1>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st);
     if (rc) return rc;
     done += kb;
     ++chunk;
