@@ -9,14 +9,14 @@
 // so every operator reduces to three "fluxes" F_a, F_b, F_c per tet and the
 // contributions -F_a, F_a-F_b, F_b-F_c, F_c to the four path vertices.
 //
-// Execution (march3): a CTA of 8 warps covers 30 node columns (x, lanes 1..30
-// of each warp) and 8 node rows (y, one warp each; warp 0 is a halo row whose
-// outputs belong to the tile below) and marches along z.  Per plane step each
-// warp loads its row of the new plane, the neighbour row above comes through
-// shared memory, x-neighbours through shuffles; each lane evaluates the six
-// tets of cell (i, j, k) and the contributions to the eight corners are
-// combined with shuffles (x) and one shared-memory exchange (y).  Every node
-// is summed by one thread in a fixed order: deterministic, no atomics.
+// Execution (march3s, march3s.cuh): a CTA of 8 warps covers 30 node columns
+// (x, lanes 1..30 of each warp) and 8 node rows (y, one warp each; warp 0 is a
+// halo row whose outputs belong to the tile below) and marches along z.  Planes
+// are staged in shared memory by cp.async two planes ahead; x-neighbours come
+// through shuffles; each lane evaluates the six tets of cell (i, j, k) and the
+// contributions to the eight corners are combined with shuffles (x) and one
+// shared-memory exchange (y).  Every node is summed by one thread in a fixed
+// order: deterministic, no atomics.
 //
 // Material word (uint32, lsg_material): bits 3m..3m+2 = n_in of tet m
 // (number of its 4 quadrature points with phi < 0), bit 18 = cell valid,
@@ -111,18 +111,6 @@ struct Elast {
       for (int q = 0; q < NOUT; ++q) c[v][q] = 0.0;
     tet<0>(u, word, c); tet<1>(u, word, c); tet<2>(u, word, c);
     tet<3>(u, word, c); tet<4>(u, word, c); tet<5>(u, word, c);
-  }
-
-  // diagonal contribution of path vertex v of tet M (component q), weight w
-  __device__ static double grad_sq(int M, int v, int q, const double *ihh, double lam_mu,
-                                   double muv) {
-    double g[3] = {0.0, 0.0, 0.0};
-    const int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
-    if (v == 0) g[a] = -ihh[a];
-    if (v == 1) { g[a] = ihh[a]; g[b] = -ihh[b]; }
-    if (v == 2) { g[b] = ihh[b]; g[cc] = -ihh[cc]; }
-    if (v == 3) g[cc] = ihh[cc];
-    return lam_mu * g[q] * g[q] + muv * (g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
   }
 };
 
@@ -348,281 +336,6 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
     } else {
       a.out[0] = tot[0];
       a.out[1] = tot[1];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// The z-marching skeleton
-// ---------------------------------------------------------------------------
-template <class PH, int ACT>
-__global__ void __launch_bounds__(kThreads, 2) march3(PH ph, Geo g, MArgs a) {
-  constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
-  constexpr int NP = Traits<ACT>::NP;
-  constexpr int NPA = NP > 0 ? NP : 1;
-  constexpr int NF = (ACT == SHAPE) ? NIN / 3 : 1;  // fields per node load
-  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
-  __shared__ double su[2][kWarps + 1][NIN][32];  // double-buffered by plane parity
-  __shared__ double sc[kWarps][2 * NOUT][32];
-  __shared__ double scratch[NPA * kWarps];
-
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nzseg = a.nzseg;
-  const int zseg = blockIdx.z % nzseg, rhs = blockIdx.z / nzseg;
-  const int nx = g.nx, ny = g.ny, nz = g.nz;
-  const int64_t nxp = nx + 1, nyp = ny + 1;
-  const int64_t plane = nxp * nyp;
-  const int64_t nn = plane * (nz + 1);
-
-  const int i = (int)blockIdx.x * kStrip - 1 + lane;
-  const int jw = (int)blockIdx.y * (kWarps - 1) - 1 + w;  // this warp's node row
-  const int jx = jw + 1;                                  // extra row (top warp only)
-  const bool top = (w == kWarps - 1);
-  const bool col_ok = ((int)blockIdx.x < a.nstrips) && i >= 0 && i <= nx;
-  const bool row_ok = jw >= 0 && jw <= ny;
-  const bool node_ok = col_ok && row_ok;
-  const bool xrow_ok = col_ok && jx <= ny;
-  const bool own = node_ok && lane >= 1 && lane <= kStrip && w >= 1;
-  const int ic = min(max(i, 0), nx);
-  const int jc = min(max(jw, 0), ny), jxc = min(jx, ny);
-  const int K0 = zseg * a.seg;
-  const int K1 = min(K0 + a.seg, nz + 1);
-  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 3;
-
-  double beta = 0.0, alpha_prev = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA) {
-    lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0 || a.finish_only) {  // CTA-uniform
-      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      const double al = s.alpha;  // pending x += alpha p of the last iteration
-      if (own) {
-        for (int kk = K0; kk < K1; ++kk) {
-          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            a.xs[voff + node * 3 + q] = fma(al, a.x2[voff + node * 3 + q], a.xs[voff + node * 3 + q]);
-        }
-      }
-      double d1[1] = {0.0}, t1[1];
-      const int nblk = gridDim.x * gridDim.y * nzseg;
-      const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk, a.counters + rhs,
-                                         blk, nblk, scratch, t1))
-        if (threadIdx.x == 0) s.reserved[1] = 0.0;
-      return;
-    }
-    first = s.first != 0.0;
-    beta = s.beta;
-    alpha_prev = s.alpha;
-  } else if constexpr (ACT == RESID) {
-    if (a.scal[rhs].done != 0.0) return;
-  }
-  const double *xin = a.x + voff;
-  const double *xin2 = (ACT == PCGA) ? a.x2 + voff : a.x;
-
-  double part[NPA];
-#pragma unroll
-  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
-
-  // node row (j, kk) -> masked input, raw value, inverse diagonal, word
-  auto load = [&](int jj, bool ok, int kk, bool write_p, double *in, double *raw, double *dg,
-                  uint32_t &wc) {
-    const int64_t node = ((int64_t)kk * nyp + jj) * nxp + ic;
-    wc = ok ? __ldg(a.words + node) : 0u;
-    if constexpr (ACT == SHAPE) {
-#pragma unroll
-      for (int f = 0; f < NF; ++f)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) in[3 * f + q] = __ldg(xin + (size_t)f * nn * 3 + node * 3 + q);
-    } else {
-      const uint32_t m = PH::mask(wc);
-      double v[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) v[q] = __ldg(xin + node * 3 + q);
-      if constexpr (HAS_DINV) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) dg[q] = __ldg(a.dinv + node * 3 + q);
-      }
-      if constexpr (ACT == PCGA) {
-        double po[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          po[q] = first ? 0.0 : __ldg(xin2 + node * 3 + q);
-          v[q] = fma(beta, po[q], v[q] * dg[q]);
-        }
-        if (write_p) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            a.y2[voff + node * 3 + q] = v[q];
-            if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
-              a.xs[voff + node * 3 + q] = fma(alpha_prev, po[q], a.xs[voff + node * 3 + q]);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        raw[q] = v[q];
-        in[q] = ((m >> q) & 1u) ? 0.0 : v[q];
-      }
-    }
-  };
-
-  auto emit = [&](int kk, uint32_t wc, const double *accv, const double *raw, const double *dg) {
-    const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
-    if constexpr (ACT == SHAPE) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        double o = accv[q];
-        if (a.accumulate) o += a.y[node * 3 + q];
-        a.y[node * 3 + q] = o;
-        if (!a.accumulate) a.y2[node * 3 + q] = accv[3 + q];
-      }
-    } else {
-      const uint32_t m = PH::mask(wc);
-      double yv[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) yv[q] = ((m >> q) & 1u) ? raw[q] : accv[q];
-      if constexpr (ACT == APPLY) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) a.y[voff + node * 3 + q] = yv[q];
-      } else if constexpr (ACT == RESID) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const double bv = __ldg(a.b + voff + node * 3 + q);
-          const double r = bv - yv[q];
-          a.y[voff + node * 3 + q] = r;
-          part[0] += bv * bv;
-          part[1] += r * r;
-          part[2] += r * (r * dg[q]);
-        }
-      } else if constexpr (ACT == PCGA) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          a.y[voff + node * 3 + q] = yv[q];
-          part[0] += raw[q] * yv[q];
-        }
-      } else if constexpr (ACT == STATS) {
-        double sp = 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const double vv = __ldg(a.x2 + node * 3 + q);
-          part[0] += raw[q] * yv[q];
-          part[1] += vv * raw[q];
-          sp += fabs(raw[q]) * g.ih[q];
-        }
-        part[2] = fmax(part[2], sp);
-      }
-    }
-  };
-
-  const int kstart = max(K0 - 1, 0);
-  const int kend = min(K1, nz);
-  // plane-k state of this warp's row (and of the row above, from smem)
-  double in_c[NIN], rt_c[NIN], iy_c[NIN], iyr_c[NIN], raw_c[3], dg_c[3], acc[NOUT];
-  uint32_t wc_c;
-  {
-    double in_t[NIN], raw_t[3], dg_t[3];
-    uint32_t wct;
-    load(jc, node_ok, kstart, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
-    if (top) {
-      load(jxc, xrow_ok, kstart, false, in_t, raw_t, dg_t, wct);
-#pragma unroll
-      for (int t = 0; t < NIN; ++t) su[kstart & 1][kWarps][t][lane] = in_t[t];
-    }
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) su[kstart & 1][w][t][lane] = in_c[t];
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      iy_c[t] = su[kstart & 1][w + 1][t][lane];
-      rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
-      iyr_c[t] = __shfl_down_sync(0xffffffffu, iy_c[t], 1);
-    }
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) acc[t] = 0.0;
-  }
-
-  for (int kk = kstart + 1; kk <= kend; ++kk) {
-    double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3];
-    uint32_t wc_n;
-    // (no barrier needed here: su is double-buffered by plane parity)
-    load(jc, node_ok, kk, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
-    if (top) {
-      double in_t[NIN], raw_t[3], dg_t[3];
-      uint32_t wct;
-      load(jxc, xrow_ok, kk, false, in_t, raw_t, dg_t, wct);
-#pragma unroll
-      for (int t = 0; t < NIN; ++t) su[kk & 1][kWarps][t][lane] = in_t[t];
-    }
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) su[kk & 1][w][t][lane] = in_n[t];
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      iy_n[t] = su[kk & 1][w + 1][t][lane];
-      rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
-      iyr_n[t] = __shfl_down_sync(0xffffffffu, iy_n[t], 1);
-    }
-    // eight corners of cell (i, jw, kk-1): bit0 = +x, bit1 = +y, bit2 = +z
-    double U[8][NIN];
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      U[0][t] = in_c[t];  U[1][t] = rt_c[t];  U[2][t] = iy_c[t];  U[3][t] = iyr_c[t];
-      U[4][t] = in_n[t];  U[5][t] = rt_n[t];  U[6][t] = iy_n[t];  U[7][t] = iyr_n[t];
-    }
-    double C[8][NOUT];
-    if constexpr (ACT == SHAPE) {
-      ph.cell(U, wc_c, own && (kk - 1) >= K0, C, part);
-    } else {
-      ph.cell(U, wc_c, i, jw, kk - 1, C);
-    }
-    // x: corners with +x belong to lane+1
-    double T[4][NOUT];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int t = 0; t < NOUT; ++t) {
-        double up = __shfl_up_sync(0xffffffffu, C[2 * q + 1][t], 1);
-        if (lane == 0) up = 0.0;
-        T[q][t] = C[2 * q][t] + up;
-      }
-    // y: corners with +y (T[1]: plane k, T[3]: plane k+1) belong to warp w+1
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) {
-      sc[w][t][lane] = T[1][t];
-      sc[w][NOUT + t][lane] = T[3][t];
-    }
-    __syncthreads();
-    double nxt[NOUT];
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) {
-      const double b0 = w > 0 ? sc[w - 1][t][lane] : 0.0;
-      const double b1 = w > 0 ? sc[w - 1][NOUT + t][lane] : 0.0;
-      acc[t] += T[0][t] + b0;
-      nxt[t] = T[2][t] + b1;
-    }
-    if (own && (kk - 1) >= K0) emit(kk - 1, wc_c, acc, raw_c, dg_c);
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      in_c[t] = in_n[t]; rt_c[t] = rt_n[t]; iy_c[t] = iy_n[t]; iyr_c[t] = iyr_n[t];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { raw_c[q] = raw_n[q]; dg_c[q] = dg_n[q]; }
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) acc[t] = nxt[t];
-    wc_c = wc_n;
-  }
-  if (K1 == nz + 1 && own && nz >= K0) emit(nz, wc_c, acc, raw_c, dg_c);
-
-  if constexpr (NP > 0) {
-    const int nblk = gridDim.x * gridDim.y * nzseg;
-    const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    double tot[NPA];
-    const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
-    if (block_partial_and_total<NP, Traits<ACT>::MAXMASK>(part, a.partials + pbase,
-                                                          a.counters + rhs, blk, nblk, scratch, tot)) {
-      if (threadIdx.x == 0) finalize<ACT>(a, rhs, tot);
     }
   }
 }
