@@ -162,8 +162,7 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
   if (!rc) rc = check_ws(ws);
   if (rc) return rc;
   if (niter < 0) { set_error("niter must be >= 0"); return LSG_ERR_ARG; }
-  return DISPATCH(op->grid, pcg_iterate(*op, *ws, niter, S(stream)),
-                  pcg_iterate(*op, *ws, niter, S(stream)));
+  return pcg_iterate_graph(*op, *ws, niter, S(stream));
 }
 
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream) {

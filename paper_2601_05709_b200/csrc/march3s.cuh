@@ -43,7 +43,6 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
   constexpr int NP = Traits<ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
   constexpr int NR = Stage<PH, ACT>::NR;
-  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *stage = reinterpret_cast<double *>(smem_raw);               // [3][kWarps+1][NR][32]
   double *xchg = stage + Stage<PH, ACT>::doubles;                      // [kWarps][2*NOUT][32]

@@ -66,6 +66,7 @@ int mesh_vertices(const lsg_grid &g, double *xyz, cudaStream_t st);
 int mesh_elements(const lsg_grid &g, int32_t *conn, cudaStream_t st);
 int transport(const lsg_grid &g, const double *phi_in, const double *theta, double dt, int nsub,
               int smooth, double h, double *phi_out, double *tmp, cudaStream_t st);
+int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
 int reinit(const lsg_grid &g, const double *phi_in, double dt, int nsub, double h, double *phi_out,
            double *tmp, double *sgn, cudaStream_t st);
 
