@@ -35,6 +35,7 @@ class Params:
     cost_tol: float = 1e-2
     prev: int = 10
     random_pars: tuple = (1, 0.05)
+    scheme: str = "explicit"  # level-set update: "explicit" (north star) or "pg" (reference)
 
 
 def adaptive_time(btt, params, rng):
@@ -105,11 +106,17 @@ def run(model, velocity, phi0, params, h, rtol=fem.CG_RTOL, on_record=None):
         if abs(dj + btt) > 1e-8 * (1.0 + abs(btt)):
             raise fem.SolverError("velocity derivative identity broke", dj + btt)
         t_end, steps = adaptive_time(btt, params, rng)
-        phi, nt = levelset.transport(grid, phi, theta, t_end, steps, params.smooth, h)
+        if params.scheme == "pg":
+            phi, nt = levelset.transport_pg(grid, phi, theta, t_end, steps, params.smooth, h), steps
+        else:
+            phi, nt = levelset.transport(grid, phi, theta, t_end, steps, params.smooth, h)
         rec["nsub_transport"] = nt
         if params.reinit_step is not None and (it + 1) % params.reinit_step == 0:
             iters_r, t_final = params.reinit_pars
-            phi, nr = levelset.reinitialize(grid, phi, int(iters_r), float(t_final), h)
+            if params.scheme == "pg":
+                phi, nr = levelset.reinitialize_pg(grid, phi, int(iters_r), float(t_final), h), int(iters_r)
+            else:
+                phi, nr = levelset.reinitialize(grid, phi, int(iters_r), float(t_final), h)
             rec["nsub_reinit"] = nr
         rec["t_end"], rec["steps"], rec["form_value"] = t_end, steps, btt
         if on_record:

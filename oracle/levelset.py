@@ -164,6 +164,85 @@ def reinitialize(grid, phi, iters, t_final, h):
     return f.reshape(-1), nsub
 
 
+# -- the reference's own scheme (restating reference ``levelset.py:109-216``) ----
+
+
+def _p1_tables(grid):
+    """Per-triangle gradients (E,3,2), areas (E,) and the edge-midpoint rule."""
+    from .fem import Space, QUAD_BARY_2D
+    s = Space(grid, 1)
+    return s, s.grads, s.measures, QUAD_BARY_2D
+
+
+def transport_tau(speed_sq, dt, h):
+    """tau = (1/2) (1/dt^2 + |v|^2/h^2)^(-1/2) (``levelset.py:121-127``)."""
+    return 0.5 / np.sqrt(1.0 / dt ** 2 + np.asarray(speed_sq) / h ** 2)
+
+
+def gradient_norm_guard(p):
+    """p / sqrt(|p|^2 + eps^2), eps = 1e-12 (1 + |p|) (``levelset.py:109-118``)."""
+    p = np.asarray(p, dtype=float)
+    mag = np.sqrt(np.sum(p * p, axis=-1, keepdims=True))
+    eps = 1e-12 * (1.0 + mag)
+    return p / np.sqrt(mag * mag + eps * eps)
+
+
+def transport_pg(grid, phi, theta, t_end, steps, smooth, h):
+    """Crank-Nicolson Petrov-Galerkin transport (``levelset.py:137-169``), 2D."""
+    import scipy.sparse.linalg as spla
+    space, g, areas, bary = _p1_tables(grid)
+    dt = t_end / steps
+    th = np.asarray(theta, dtype=float).reshape(-1, 2)[grid.elements]  # (E,3,2)
+    th_q = np.einsum("qi,tic->tqc", bary, th)
+    tau = transport_tau(np.sum(th_q * th_q, axis=2), dt, h)
+    conv = np.einsum("tqd,tid->tqi", th_q, g)
+    hat = bary[None, :, :] + tau[:, :, None] * conv
+    w = space.quad_weights
+    m_hat = np.einsum("tq,tqa,qb->tab", w, hat, bary)
+    half = 0.5 * np.einsum("tq,tqa,tqb->tab", w, hat, conv)
+    if smooth:
+        half = half + 0.5 * h * h * np.einsum("t,tad,tbd->tab", areas, g, g)
+    lhs = space.assemble_matrix(m_hat + dt * half)
+    rhs = space.assemble_matrix(m_hat - dt * half)
+    lu = spla.splu(lhs.tocsc())
+    vals = np.asarray(phi, dtype=float).copy()
+    for _ in range(steps):
+        vals = lu.solve(rhs @ vals)
+    return vals
+
+
+def reinitialize_pg(grid, phi, iters, t_final, h):
+    """Petrov-Galerkin Euler/AB2 reinitialisation (``levelset.py:172-216``), 2D."""
+    import scipy.sparse.linalg as spla
+    space, g, areas, bary = _p1_tables(grid)
+    dt = t_final / iters
+    phi = np.asarray(phi, dtype=float)
+    s_q = np.einsum("qi,ti->tq", bary, phi[grid.elements])
+    s_q = s_q / np.sqrt(s_q * s_q + h * h)
+    tau = transport_tau(s_q * s_q, dt, h)
+    w = space.quad_weights
+    cur = phi.copy()
+    grad_cur = space.grad_at_quad(cur)
+    grad_prev = grad_cur
+    for _ in range(iters):
+        direction = gradient_norm_guard(grad_cur)
+        vel = s_q[:, :, None] * direction[:, None, :]
+        conv = np.einsum("tqd,tid->tqi", vel, g)
+        hat = bary[None, :, :] + tau[:, :, None] * conv
+        m_hat = space.assemble_matrix(np.einsum("tq,tqa,qb->tab", w, hat, bary))
+        lu = spla.splu(m_hat.tocsc())
+        mag_cur = np.linalg.norm(grad_cur, axis=1)
+        mag_prev = np.linalg.norm(grad_prev, axis=1)
+        hamiltonian = 0.5 * s_q * (mag_prev - 3.0 * mag_cur)[:, None]
+        load = np.einsum("tq,tqa->ta", w * (hamiltonian + s_q), hat)
+        diffusion = 0.5 * h * h * np.einsum("t,td,tad->ta", areas, grad_prev - 3.0 * grad_cur, g)
+        rhs = m_hat @ cur + dt * space.assemble_vector(load + diffusion)
+        cur = lu.solve(rhs)
+        grad_prev = grad_cur
+        grad_cur = space.grad_at_quad(cur)
+    return cur
+
+
 # -- diagnostics (restating reference ``levelset.py:222-278``) -----------------
 
 

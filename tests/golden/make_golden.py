@@ -21,7 +21,7 @@ if REF not in sys.path:
     sys.path.insert(0, REF)
 
 from lsopt import driver as ldriver  # noqa: E402
-from lsopt.fem import (DirichletSet, FunctionSpace, SparseSystem, apply_dirichlet,  # noqa: E402
+from lsopt.fem import (DirichletSet, FemField, FunctionSpace, SparseSystem, apply_dirichlet,  # noqa: E402
                        elasticity_matrix, vector_load)
 from lsopt.levelset import LevelSetField  # noqa: E402
 from lsopt.mesh import build_rect_mesh, mesh_diameter  # noqa: E402
@@ -144,6 +144,40 @@ def main():
     at = [ldriver.adaptive_time(b, params, r) for b in (0.2, 0.05, 3.0, 1e-9, 17.0, 0.6)]
     g["adaptive_btt"] = np.array([0.2, 0.05, 3.0, 1e-9, 17.0, 0.6])
     g["adaptive_out"] = np.array(at, dtype=float)
+
+    # -- the reference's own level-set scheme (levelset.py:137-216) ----------------------
+    from lsopt.levelset import reinitialize, transport
+
+    sq = build_rect_mesh((0.0, 0.0, 1.0, 1.0), 24, 20)
+    s1sp, s2sp = FunctionSpace(sq, 1), FunctionSpace(sq, 2)
+    phi_sq = LevelSetField.from_field(
+        s1sp.interpolate(lambda p: np.hypot(p[:, 0] - 0.45, p[:, 1] - 0.55) - 0.3 + 0.05 * np.sin(5 * p[:, 0])))
+    th_sq = s2sp.interpolate(lambda p: np.stack([np.sin(np.pi * p[:, 0]) * np.cos(2 * p[:, 1]),
+                                                 0.3 + p[:, 0] * p[:, 1]], axis=1))
+    g["ls_phi"] = phi_sq.values
+    g["ls_theta"] = th_sq.values
+    g["ls_transport"] = transport(phi_sq, th_sq, 0.03, 8, smooth=False).values
+    g["ls_transport_smooth"] = transport(phi_sq, th_sq, 0.03, 8, smooth=True).values
+    g["ls_reinit"] = reinitialize(LevelSetField(FemField(s1sp, 3.0 * phi_sq.values), phi_sq.h),
+                                  8, 0.1).values
+
+    # -- a full reference run() on the cfg1 geometry at 40x20 (driver.py:211-298) -----
+    from lsopt.driver import RunParams, run
+
+    rules = [(1, lambda p: p[:, 0] < 1e-12),
+             (2, lambda p: (p[:, 0] > 2.0 - 1e-12) & (p[:, 1] >= 0.45) & (p[:, 1] <= 0.55))]
+    m40 = build_rect_mesh((0.0, 0.0, 2.0, 1.0), 40, 20, rules)
+    model40 = ComplianceModel(m40, 1, 2, (0.0, -1.0), 1.0, lame=LAME, bilinear=bil)
+    model40.material = MaterialIndicator(1.0, ERSATZ)
+    phi40 = LevelSetField.from_field(FunctionSpace(m40, 1).interpolate(phi_fn))
+    params = RunParams(niter=12, start_to_check=12, reinit_step=5, reinit_pars=(8, 0.1))
+    _, hist = run(model40, phi40, params, timing=False)
+    g["run_cost"] = np.array([r.cost for r in hist])
+    g["run_constraint"] = np.array([float(r.constraint[0]) for r in hist])
+    g["run_lagrangian"] = np.array([r.lagrangian for r in hist])
+    g["run_t_end"] = np.array([r.t_end for r in hist])
+    g["run_steps"] = np.array([r.steps for r in hist])
+    g["run_form_value"] = np.array([r.form_value for r in hist])
 
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, sum(v.nbytes for v in g.values()) / 1e6, "MB raw")

@@ -126,6 +126,35 @@ class TestComplianceKAT:
         assert plus.cost(phi, states) == pytest.approx(golden["plus_J"][0], rel=1e-9)
 
 
+class TestReferenceScheme:
+    """The reference's CN/PG transport and PG/AB2 reinit (levelset.py:137-216), restated."""
+
+    def test_transport_and_reinit(self, golden):
+        g = Grid((0.0, 0.0), (1.0, 1.0), (24, 20))
+        h = level_set_h(g)
+        for smooth, key in ((False, "ls_transport"), (True, "ls_transport_smooth")):
+            out = levelset.transport_pg(g, golden["ls_phi"], golden["ls_theta"], 0.03, 8, smooth, h)
+            assert rel_l2(out, golden[key]) <= 1e-13
+        out = levelset.reinitialize_pg(g, 3.0 * golden["ls_phi"], 8, 0.1, h)
+        assert rel_l2(out, golden["ls_reinit"]) <= 1e-13
+
+    def test_full_loop_matches_reference_run(self, golden):
+        """Oracle loop with the reference scheme vs the reference's own run()
+        (cfg1 geometry at 40x20, 12 iterations, reinit every 5)."""
+        from oracle import cases as ocases
+        from paper_2601_05709_b200 import configs
+        c = configs.case("cfg1", scale=4)
+        c = type(c)(**{**c.__dict__, "niter": 12, "reinit_step": 5})
+        grid, om, ovel, phi0, params, h = ocases.build(c)
+        params = odriver.Params(**{**params.__dict__, "scheme": "pg"})
+        _, hist = odriver.run(om, ovel, phi0, params, h)
+        np.testing.assert_allclose([r["cost"] for r in hist], golden["run_cost"], rtol=1e-8)
+        np.testing.assert_allclose([r["constraint"][0] for r in hist], golden["run_constraint"], rtol=1e-12)
+        np.testing.assert_allclose([r["lagrangian"] for r in hist], golden["run_lagrangian"], rtol=1e-8)
+        np.testing.assert_allclose([r["t_end"] for r in hist], golden["run_t_end"], rtol=1e-8)
+        np.testing.assert_array_equal([r["steps"] for r in hist], golden["run_steps"])
+
+
 class TestHostKAT:
     def test_ppl_table(self, golden):
         st = ppl_init(1)
