@@ -52,6 +52,15 @@ typedef struct {
 /* Operator kinds for lsg_op. */
 #define LSG_OP_ELASTICITY 1 /* ersatz-material linear elasticity (fem.py:397-411) */
 #define LSG_OP_H1 2         /* velocity form, velocity.py:98-127 */
+/* The reference's own level-set scheme (2D), non-symmetric step operators:
+ *   PG_TRANSPORT: m_hat + sign*dt*half of levelset.py:150-164; p0 = dt,
+ *                 p1 = h, p2 = sign (+1 left / -1 right), p3 = smooth;
+ *                 aux[0] = theta (2N).
+ *   PG_REINIT:    m_hat of levelset.py:196-204; p0 = dt, p1 = h;
+ *                 aux[0] = phi0 (frozen sign), aux[1] = current iterate,
+ *                 aux[2] = previous iterate (lsg_pg_reinit_rhs only). */
+#define LSG_OP_PG_TRANSPORT 3
+#define LSG_OP_PG_REINIT 4
 
 /* Matrix-free operator description.
  *   ELASTICITY: words = per-node material word written by lsg_material
@@ -70,6 +79,7 @@ typedef struct {
   lsg_grid grid;
   const void *words;
   double p[6];
+  const double *aux[4]; /* auxiliary device fields (PG operators), else NULL */
 } lsg_op;
 
 /* Per right-hand-side PCG scalars (device memory, 16 doubles each). */
@@ -225,6 +235,18 @@ int lsg_transport(const lsg_grid *g, const double *phi_in, const double *theta, 
                   void *stream);
 int lsg_reinit(const lsg_grid *g, const double *phi_in, double dt, int32_t nsub, double h,
                double *phi_out, double *tmp, double *sgn, void *stream);
+
+/* Reference-scheme reinitialisation right-hand side (levelset.py:205-212):
+ * rhs = m_hat cur + dt (load + diffusion), PG_REINIT operator (aux[0..2]). */
+int lsg_pg_reinit_rhs(const lsg_op *op, double *rhs, void *stream);
+
+/* Right-Jacobi-preconditioned BiCGStab for a PG operator: A x = b to
+ * ||r|| <= rtol ||b|| (x holds the initial guess).  Unlike the other entry
+ * points it synchronises `stream` once per iteration to test convergence.
+ * work: lsg_bicgstab_work_doubles(g) doubles of device memory. */
+int64_t lsg_bicgstab_work_doubles(const lsg_grid *g);
+int lsg_bicgstab(const lsg_op *op, const double *b, double *x, double *work, double rtol,
+                 int32_t maxit, int32_t *iters, double *resid, void *stream);
 
 /* max_i sum_d |v_d,i| / h_d over a vector field (CFL speed), out: 1 double. */
 int lsg_cfl_speed(const lsg_grid *g, const double *v, double *out, double *partials,

@@ -21,6 +21,8 @@ LSG_ERR_ARG = -1
 LSG_ERR_CUDA = -2
 LSG_OP_ELASTICITY = 1
 LSG_OP_H1 = 2
+LSG_OP_PG_TRANSPORT = 3
+LSG_OP_PG_REINIT = 4
 
 SCAL_FIELDS = ("atol", "rho", "alpha", "beta", "rr", "pq", "bb", "iters", "done", "zero_rhs",
                "maxiter", "first", "rz_new")
@@ -38,7 +40,8 @@ class Grid(ctypes.Structure):
 
 class Op(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("pad_", ctypes.c_int32), ("grid", Grid),
-                ("words", ctypes.c_void_p), ("p", ctypes.c_double * 6)]
+                ("words", ctypes.c_void_p), ("p", ctypes.c_double * 6),
+                ("aux", ctypes.c_void_p * 4)]
 
 
 class PcgWs(ctypes.Structure):
@@ -83,6 +86,10 @@ SIGNATURES = {
     "lsg_transport": (ctypes.c_int, [_G, _P, _P, _D, _I, _I, _D, _P, _P, _P]),
     "lsg_reinit": (ctypes.c_int, [_G, _P, _D, _I, _D, _P, _P, _P, _P]),
     "lsg_cfl_speed": (ctypes.c_int, [_G, _P, _P, _P, _P, _P]),
+    "lsg_pg_reinit_rhs": (ctypes.c_int, [_O, _P, _P]),
+    "lsg_bicgstab_work_doubles": (ctypes.c_int64, [_G]),
+    "lsg_bicgstab": (ctypes.c_int, [_O, _P, _P, _P, _D, _I, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(ctypes.c_double), _P]),
 }
 
 _lib = None
@@ -142,13 +149,15 @@ def make_grid(dim, n, lo, hi):
     return g
 
 
-def make_op(kind, grid, words, params):
+def make_op(kind, grid, words, params, aux=()):
     op = Op()
     op.kind = kind
     op.grid = grid
-    op.words = words.data_ptr()
+    op.words = words.data_ptr() if words is not None else None
     for i in range(6):
         op.p[i] = float(params[i]) if i < len(params) else 0.0
+    for i, t in enumerate(aux):
+        op.aux[i] = t.data_ptr() if t is not None else None
     return op
 
 

@@ -47,12 +47,25 @@ static int check_op(const lsg_op *op) {
   if (!op) { set_error("null operator"); return LSG_ERR_ARG; }
   int rc = check_grid(&op->grid);
   if (rc) return rc;
+  if (op->kind == LSG_OP_PG_TRANSPORT || op->kind == LSG_OP_PG_REINIT) {
+    if (op->grid.dim != 2) { set_error("the reference (PG) level-set scheme is 2D only"); return LSG_ERR_ARG; }
+    if (!op->aux[0] || (op->kind == LSG_OP_PG_REINIT && !op->aux[1])) {
+      set_error("PG operator fields missing");
+      return LSG_ERR_ARG;
+    }
+    if (!(op->p[0] > 0.0) || !(op->p[1] > 0.0)) { set_error("PG operator needs dt > 0 and h > 0"); return LSG_ERR_ARG; }
+    return LSG_OK;
+  }
   if (op->kind != LSG_OP_ELASTICITY && op->kind != LSG_OP_H1) {
     set_error("unknown operator kind %d", op->kind);
     return LSG_ERR_ARG;
   }
   if (!op->words) { set_error("operator words missing"); return LSG_ERR_ARG; }
   return LSG_OK;
+}
+
+static bool is_pg(const lsg_op *op) {
+  return op->kind == LSG_OP_PG_TRANSPORT || op->kind == LSG_OP_PG_REINIT;
 }
 
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
@@ -124,13 +137,47 @@ int lsg_apply(const lsg_op *op, int32_t k, const double *x, double *y, void *str
   int rc = check_op(op);
   if (rc) return rc;
   if (k < 1 || k > 65535) { set_error("batch size k must be in [1, 65535], got %d", k); return LSG_ERR_ARG; }
+  if (is_pg(op)) {
+    if (k != 1) { set_error("PG operators apply to one field"); return LSG_ERR_ARG; }
+    return pg::apply(*op, x, y, S(stream));
+  }
   return DISPATCH(op->grid, apply(*op, k, x, y, S(stream)), apply(*op, k, x, y, S(stream)));
 }
 
 int lsg_diag(const lsg_op *op, double *diag_out, void *stream) {
   int rc = check_op(op);
   if (rc) return rc;
+  if (is_pg(op)) return pg::diag(*op, diag_out, S(stream));
   return DISPATCH(op->grid, diag(*op, diag_out, S(stream)), diag(*op, diag_out, S(stream)));
+}
+
+int lsg_pg_reinit_rhs(const lsg_op *op, double *rhs, void *stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  if (op->kind != LSG_OP_PG_REINIT || !op->aux[2]) {
+    set_error("lsg_pg_reinit_rhs needs a PG_REINIT operator with aux[2] = previous iterate");
+    return LSG_ERR_ARG;
+  }
+  return pg::reinit_rhs(*op, rhs, S(stream));
+}
+
+int64_t lsg_bicgstab_work_doubles(const lsg_grid *g) {
+  if (check_grid(g)) return -1;
+  int64_t nn = 1;
+  for (int a = 0; a < g->dim; ++a) nn *= (int64_t)g->n[a] + 1;
+  return 9 * nn + 16 + 2 * 296 + 8;
+}
+
+int lsg_bicgstab(const lsg_op *op, const double *b, double *x, double *work, double rtol,
+                 int32_t maxit, int32_t *iters, double *resid, void *stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  if (!is_pg(op)) { set_error("lsg_bicgstab solves the PG level-set operators"); return LSG_ERR_ARG; }
+  if (!b || !x || !work || !iters || !resid || maxit < 0) { set_error("bad BiCGStab arguments"); return LSG_ERR_ARG; }
+  int it = 0;
+  rc = pg::bicgstab(*op, b, x, work, rtol, maxit, &it, resid, S(stream));
+  *iters = it;
+  return rc;
 }
 
 int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream) {

@@ -67,6 +67,14 @@ int mesh_elements(const lsg_grid &g, int32_t *conn, cudaStream_t st);
 int transport(const lsg_grid &g, const double *phi_in, const double *theta, double dt, int nsub,
               int smooth, double h, double *phi_out, double *tmp, cudaStream_t st);
 int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
+
+namespace pg {  // the reference's own level-set scheme, 2D (pg2d.cu)
+int apply(const lsg_op &op, const double *x, double *y, cudaStream_t st);
+int diag(const lsg_op &op, double *d, cudaStream_t st);
+int reinit_rhs(const lsg_op &op, double *rhs, cudaStream_t st);
+int bicgstab(const lsg_op &op, const double *b, double *x, double *work, double rtol, int maxit,
+             int *iters, double *resid, cudaStream_t st);
+}  // namespace pg
 int reinit(const lsg_grid &g, const double *phi_in, double dt, int nsub, double h, double *phi_out,
            double *tmp, double *sgn, cudaStream_t st);
 

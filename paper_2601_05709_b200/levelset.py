@@ -14,6 +14,7 @@ the device (``csrc/levelset.cu``; statement and CPU oracle in
   kappa) / CFL)).
 """
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -149,13 +150,73 @@ def _check_velocity_field(phi, theta):
         raise ConfigError("velocity and level set use different meshes")
 
 
-def transport(phi, theta, t_end, steps, smooth=False):
-    """Advect phi along theta for time t_end (``levelset.py:137-169`` signature)."""
+PG_RTOL = 1e-14  # BiCGStab tolerance of the reference scheme's step solves (reference: SuperLU)
+
+
+def _bicgstab(op, b, x, mesh):
+    work = _SCRATCH.get(mesh, "bicg_work", int(_lib.load().lsg_bicgstab_work_doubles(mesh.grid)))
+    iters = ctypes.c_int32(0)
+    resid = ctypes.c_double(0.0)
+    _lib.call("lsg_bicgstab", op, _lib.ptr(b), _lib.ptr(x), _lib.ptr(work), PG_RTOL, 2000,
+              ctypes.byref(iters), ctypes.byref(resid), _lib.stream())
+    return int(iters.value)
+
+
+def _transport_pg(phi, theta, t_end, steps, smooth):
+    """Crank-Nicolson Petrov-Galerkin transport (``levelset.py:137-169``) on the device."""
+    mesh = phi.mesh
+    if mesh.dim != 2:
+        raise ConfigError("the reference (pg) level-set scheme is 2D only")
+    dt = t_end / steps
+    th = theta.values
+    lhs = _lib.make_op(_lib.LSG_OP_PG_TRANSPORT, mesh.grid, None, (dt, phi.h, 1.0, float(smooth)), (th,))
+    rhs = _lib.make_op(_lib.LSG_OP_PG_TRANSPORT, mesh.grid, None, (dt, phi.h, -1.0, float(smooth)), (th,))
+    vals = phi.values.clone()
+    b = torch.empty_like(vals)
+    for _ in range(steps):
+        _lib.call("lsg_apply", rhs, 1, _lib.ptr(vals), _lib.ptr(b), _lib.stream())
+        _bicgstab(lhs, b, vals, mesh)
+    out = LevelSetField(FemField(phi.space, vals), phi.h)
+    out.substeps = steps
+    return out
+
+
+def _reinitialize_pg(phi, iters, t_final):
+    """Petrov-Galerkin Euler/AB2 reinitialisation (``levelset.py:172-216``) on the device."""
+    mesh = phi.mesh
+    if mesh.dim != 2:
+        raise ConfigError("the reference (pg) level-set scheme is 2D only")
+    dt = t_final / iters
+    phi0 = phi.values
+    cur, prev = phi0.clone(), phi0.clone()  # duplicated history: step one is Euler
+    b = torch.empty_like(cur)
+    for _ in range(iters):
+        op = _lib.make_op(_lib.LSG_OP_PG_REINIT, mesh.grid, None, (dt, phi.h), (phi0, cur, prev))
+        _lib.call("lsg_pg_reinit_rhs", op, _lib.ptr(b), _lib.stream())
+        x = cur.clone()
+        _bicgstab(op, b, x, mesh)
+        prev, cur = cur, x
+    out = LevelSetField(FemField(phi.space, cur), phi.h)
+    out.substeps = iters
+    return out
+
+
+def transport(phi, theta, t_end, steps, smooth=False, scheme="explicit"):
+    """Advect phi along theta for time t_end (``levelset.py:137-169`` signature).
+
+    ``scheme="explicit"`` (default): the north star's explicit upwind HJ
+    step under CFL; ``scheme="pg"``: the reference's own Crank-Nicolson
+    Petrov-Galerkin step (2D).
+    """
     if t_end <= 0.0:
         raise ConfigError(f"transport needs t_end > 0, got {t_end}")
     if steps < 1:
         raise ConfigError(f"transport needs steps >= 1, got {steps}")
     _check_velocity_field(phi, theta)
+    if scheme == "pg":
+        return _transport_pg(phi, theta, t_end, steps, smooth)
+    if scheme != "explicit":
+        raise ConfigError(f"unknown level-set scheme {scheme!r}")
     mesh = phi.mesh
     nsub = transport_substeps(mesh, cfl_speed(theta), t_end, steps, smooth, phi.h)
     n = mesh.num_vertices
@@ -169,12 +230,16 @@ def transport(phi, theta, t_end, steps, smooth=False):
     return res
 
 
-def reinitialize(phi, iters, t_final):
+def reinitialize(phi, iters, t_final, scheme="explicit"):
     """Drive phi toward the signed distance of its zero set (``levelset.py:172-216`` signature)."""
     if iters < 2:
         raise ConfigError(f"reinitialization needs iters >= 2, got {iters}")
     if t_final <= 0.0:
         raise ConfigError(f"reinitialization needs t_final > 0, got {t_final}")
+    if scheme == "pg":
+        return _reinitialize_pg(phi, iters, t_final)
+    if scheme != "explicit":
+        raise ConfigError(f"unknown level-set scheme {scheme!r}")
     mesh = phi.mesh
     nsub = reinit_substeps(mesh, iters, t_final, phi.h)
     n = mesh.num_vertices

@@ -247,3 +247,39 @@ class TestHistory:
             assert r.steps == o["steps"]
             assert r.transport_substeps == o["nsub_transport"]
             assert r.reinit_substeps == o["nsub_reinit"]
+
+
+class TestReferenceScheme:
+    """The reference's own CN/PG transport and PG/AB2 reinit on the device
+    (levelset.py:137-216) vs the reference's outputs, and a full run() with it
+    vs the reference's own run() history (tests/golden/make_golden.py)."""
+
+    def _sq(self, golden):
+        mesh = build_rect_mesh((0.0, 0.0, 1.0, 1.0), 24, 20)
+        phi = LevelSetField.from_field(FemField(FunctionSpace(mesh, 1), golden["ls_phi"]))
+        th = FemField(FunctionSpace(mesh, 2), golden["ls_theta"])
+        return mesh, phi, th
+
+    @pytest.mark.parametrize("smooth,key", [(False, "ls_transport"), (True, "ls_transport_smooth")])
+    def test_transport_vs_reference(self, golden, smooth, key):
+        mesh, phi, th = self._sq(golden)
+        out = transport(phi, th, 0.03, 8, smooth, scheme="pg")
+        assert rel_l2(host(out.values), golden[key]) <= 1e-10
+        np.testing.assert_array_equal(host(phi.values), golden["ls_phi"])
+
+    def test_reinit_vs_reference(self, golden):
+        mesh, phi, th = self._sq(golden)
+        p3 = LevelSetField(FemField(phi.space, 3.0 * phi.values), phi.h)
+        out = reinitialize(p3, 8, 0.1, scheme="pg")
+        assert rel_l2(host(out.values), golden["ls_reinit"]) <= 1e-10
+
+    def test_run_history_vs_reference_run(self, golden):
+        c = configs.case("cfg1", scale=4)
+        c = type(c)(**{**c.__dict__, "niter": 12, "reinit_step": 5})
+        mesh, model, phi, params = configs.build(c)
+        params = lsg.RunParams(**{**params.__dict__, "level_set_scheme": "pg"})
+        _, hist = lsg.run(model, phi, params, timing=False)
+        np.testing.assert_allclose([r.cost for r in hist], golden["run_cost"], rtol=1e-4)
+        np.testing.assert_allclose([r.constraint[0] for r in hist], golden["run_constraint"], rtol=1e-4)
+        np.testing.assert_allclose([r.t_end for r in hist], golden["run_t_end"], rtol=1e-4)
+        np.testing.assert_array_equal([r.steps for r in hist], golden["run_steps"])
