@@ -179,6 +179,20 @@ def main():
     g["run_steps"] = np.array([r.steps for r in hist])
     g["run_form_value"] = np.array([r.form_value for r in hist])
 
+    # -- output formats (output.py:23-124): bytes of the reference writers ---------------
+    import tempfile
+
+    from lsopt.output import write_history_csv, write_vtk
+
+    with tempfile.TemporaryDirectory() as tmp:
+        write_history_csv(os.path.join(tmp, "h.csv"), hist)
+        g["run_history_csv"] = np.array(open(os.path.join(tmp, "h.csv")).read())
+        m32 = build_rect_mesh((0.0, 0.0, 2.0, 1.0), 3, 2)
+        f1 = FunctionSpace(m32, 1).interpolate(lambda p: np.sin(p[:, 0]) - p[:, 1] / 3.0)
+        f2 = FunctionSpace(m32, 2).interpolate(lambda p: np.stack([p[:, 0] / 7.0, -p[:, 1]], 1))
+        write_vtk(m32, {"phi": f1, "theta": f2}, os.path.join(tmp, "m.vtk"))
+        g["vtk_text"] = np.array(open(os.path.join(tmp, "m.vtk")).read())
+
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, sum(v.nbytes for v in g.values()) / 1e6, "MB raw")
 

@@ -283,3 +283,24 @@ class TestReferenceScheme:
         np.testing.assert_allclose([r.constraint[0] for r in hist], golden["run_constraint"], rtol=1e-4)
         np.testing.assert_allclose([r.t_end for r in hist], golden["run_t_end"], rtol=1e-4)
         np.testing.assert_array_equal([r.steps for r in hist], golden["run_steps"])
+
+
+class TestOutput:
+    def test_vtk_bytes_match_reference(self, golden, tmp_path):
+        from paper_2601_05709_b200.output import write_vtk
+        m = build_rect_mesh((0.0, 0.0, 2.0, 1.0), 3, 2)
+        f1 = FunctionSpace(m, 1).interpolate(lambda p: np.sin(p[:, 0]) - p[:, 1] / 3.0)
+        f2 = FunctionSpace(m, 2).interpolate(lambda p: np.stack([p[:, 0] / 7.0, -p[:, 1]], 1))
+        write_vtk(m, {"phi": f1, "theta": f2}, tmp_path / "m.vtk")
+        assert (tmp_path / "m.vtk").read_text() == str(golden["vtk_text"])
+
+    def test_streaming_history_writer(self, tmp_path):
+        from paper_2601_05709_b200.output import HistoryWriter, history_header
+        c = configs.case("cfg1", scale=8)
+        c = type(c)(**{**c.__dict__, "niter": 3})
+        mesh, model, phi, params = configs.build(c)
+        with HistoryWriter(tmp_path / "h.csv") as w:
+            _, hist = lsg.run(model, phi, params, on_record=w.on_record, timing=False)
+        lines = (tmp_path / "h.csv").read_text().strip().split("\n")
+        assert lines[0] == history_header(1) and len(lines) == 4
+        assert float(lines[1].split(",")[1]) == hist[0].cost
