@@ -33,7 +33,7 @@ struct Stage {
   static constexpr int NOUT = PH::NOUT;
   static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NR * 32;
   static constexpr size_t words = (size_t)3 * (kWarps + 1) * 32;
-  static constexpr size_t xchg = (size_t)kWarps * 2 * NOUT * 32;
+  static constexpr size_t xchg = (size_t)2 * kWarps * 2 * NOUT * 32;  // double-buffered
   static constexpr size_t bytes = doubles * 8 + xchg * 8 + words * 4;
 };
 
@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
   auto SW = [&](int slot, int row, int l) -> uint32_t & {
     return stw[((size_t)slot * (kWarps + 1) + row) * 32 + l];
   };
-  auto SC = [&](int wr, int t, int l) -> double & { return xchg[((size_t)wr * 2 * NOUT + t) * 32 + l]; };
+  auto SC = [&](int par, int wr, int t, int l) -> double & {
+    return xchg[(((size_t)par * kWarps + wr) * 2 * NOUT + t) * 32 + l];
+  };
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nzseg = a.nzseg;
@@ -258,12 +260,14 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
     }
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) acc[t] = 0.0;
+    cp_async_wait<1>();  // plane kstart+1 has landed
+    __syncthreads();     // ... for every thread
   }
 
+  // One barrier per plane: it publishes both this step's y-contributions
+  // (exchange buffer double-buffered by parity) and the staged plane kk+1.
   for (int kk = kstart + 1; kk <= kend; ++kk) {
-    cp_async_wait<1>();  // plane kk has landed (kk+1 may still be in flight)
-    __syncthreads();     // ... for every thread; slot (kk-1)%3 is no longer read
-    issue(kk + 2, (kk + 2) % 3);
+    issue(kk + 2, (kk + 2) % 3);  // slot of plane kk-1, fully read before the last barrier
     const int sl = kk % 3;
     double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3], raw_t[3], dg_t[3];
     uint32_t wc_n, wt;
@@ -295,17 +299,19 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
         if (lane == 0) up = 0.0;
         T[q][t] = C[2 * q][t] + up;
       }
+    const int par = kk & 1;
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) {
-      SC(w, t, lane) = T[1][t];
-      SC(w, NOUT + t, lane) = T[3][t];
+      SC(par, w, t, lane) = T[1][t];
+      SC(par, w, NOUT + t, lane) = T[3][t];
     }
+    cp_async_wait<1>();  // plane kk+1 has landed (kk+2 may still be in flight)
     __syncthreads();
     double nxt[NOUT];
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) {
-      const double b0 = w > 0 ? SC(w - 1, t, lane) : 0.0;
-      const double b1 = w > 0 ? SC(w - 1, NOUT + t, lane) : 0.0;
+      const double b0 = w > 0 ? SC(par, w - 1, t, lane) : 0.0;
+      const double b1 = w > 0 ? SC(par, w - 1, NOUT + t, lane) : 0.0;
       acc[t] += T[0][t] + b0;
       nxt[t] = T[2][t] + b1;
     }
