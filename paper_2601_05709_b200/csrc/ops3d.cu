@@ -114,6 +114,67 @@ struct Elast {
   }
 };
 
+// Cubic cells (h_x = h_y = h_z, cfg3 and cfg5): the fluxes are the columns of
+// the symmetric stress scaled by one 1/h, so with s = w mu/h^2, l = w lam/h^2
+//   T_d[q] = s (D_d[q] + D_q[d])  (q != d, shared by T_d and T_q),
+//   T_d[d] = 2 s D_d[d] + l (D_0[0] + D_1[1] + D_2[2]),
+// the weight is folded into s and l, and each corner's first contribution is
+// a plain write (compile-time first-touch), about 20% fewer fp64 instructions
+// per cell than the general form above.
+struct ElastC {
+  static constexpr int NIN = 3, NOUT = 3;
+  double w0, w1;  // |T| (inside n + outside (4-n)) / 4 = w0 + w1 n
+  double cs, cl;  // mu / h^2, lam / h^2
+  __device__ __forceinline__ static bool valid(uint32_t w) { return Elast::valid(w); }
+  __device__ __forceinline__ static uint32_t mask(uint32_t w) { return Elast::mask(w); }
+
+  // does a tet with index < M touch corner v?
+  static __host__ __device__ constexpr bool touched(int M, int v) {
+    return M > 0 && (v == 0 || v == 7 || corner(M - 1, 1) == v || corner(M - 1, 2) == v ||
+                     touched(M - 1, v));
+  }
+  template <int M, int V>
+  __device__ __forceinline__ static void put(double (*c)[NOUT], int q, double x) {
+    if constexpr (touched(M, V)) c[V][q] += x; else c[V][q] = x;
+  }
+
+  template <int M>
+  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT]) const {
+    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
+    const double w = valid(word) ? fma((double)((word >> (3 * M)) & 7u), w1, w0) : 0.0;
+    const double s = w * cs, l = w * cl;
+    double D[3][3];  // D[axis][comp]
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      D[a][q] = u[P1][q] - u[P0][q];
+      D[b][q] = u[P2][q] - u[P1][q];
+      D[cc][q] = u[P3][q] - u[P2][q];
+    }
+    const double lt = l * (D[0][0] + D[1][1] + D[2][2]);
+    const double s2 = s + s;
+    double T[3][3];
+    T[0][1] = T[1][0] = s * (D[0][1] + D[1][0]);
+    T[0][2] = T[2][0] = s * (D[0][2] + D[2][0]);
+    T[1][2] = T[2][1] = s * (D[1][2] + D[2][1]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) T[d][d] = fma(s2, D[d][d], lt);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      put<M, P0>(c, q, -T[a][q]);
+      put<M, P1>(c, q, T[a][q] - T[b][q]);
+      put<M, P2>(c, q, T[b][q] - T[cc][q]);
+      put<M, P3>(c, q, T[cc][q]);
+    }
+  }
+
+  __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int, int, int,
+                                       double (*c)[NOUT]) const {
+    tet<0>(u, word, c); tet<1>(u, word, c); tet<2>(u, word, c);
+    tet<3>(u, word, c); tet<4>(u, word, c); tet<5>(u, word, c);
+  }
+};
+
 struct H1 {
   static constexpr int NIN = 3, NOUT = 3;
   int nx, ny, nz;
@@ -688,6 +749,20 @@ static Elast make_elast(const Geo &g, const lsg_op &op) {
   return e;
 }
 
+static bool is_cubic(const Geo &g) {
+  return fabs(g.h[1] - g.h[0]) <= 1e-14 * g.h[0] && fabs(g.h[2] - g.h[0]) <= 1e-14 * g.h[0];
+}
+
+static ElastC make_elast_cubic(const Geo &g, const lsg_op &op) {
+  const Elast e = make_elast(g, op);
+  ElastC c;
+  c.w0 = e.w0;
+  c.w1 = e.w1;
+  c.cs = e.A[0];
+  c.cl = e.lam * g.ih[0] * g.ih[0];
+  return c;
+}
+
 static H1 make_h1(const Geo &g, const lsg_op &op) {
   H1 h;
   const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
@@ -746,7 +821,10 @@ template <int ACT>
 static int dispatch(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   a.words = static_cast<const uint32_t *>(op.words);
-  if (op.kind == LSG_OP_ELASTICITY) return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_ELASTICITY) {
+    if (is_cubic(g)) return launch<ElastC, ACT>(make_elast_cubic(g, op), g, a, k, st);
+    return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
+  }
   if (op.kind == LSG_OP_H1) return launch<H1, ACT>(make_h1(g, op), g, a, k, st);
   set_error("unknown operator kind %d", op.kind);
   return LSG_ERR_ARG;
