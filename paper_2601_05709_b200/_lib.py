@@ -14,7 +14,7 @@ import torch
 
 from .errors import ConfigError, SolverError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblsgpu.so")
+LIB_PATH = os.environ.get("LSG_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblsgpu.so")
 
 LSG_OK = 0
 LSG_ERR_ARG = -1

@@ -21,35 +21,50 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// doubles staged per node: APPLY/STATS: input (3); RESID: x, dinv (6);
-// PCGA: r, p_old, dinv, x (12); SHAPE: KB states (3 KB)
+// Node vectors are interleaved [node][3], so the 32 nodes of a warp row are
+// one contiguous window of <= 768 bytes per source array.  It is staged
+// verbatim with 16-byte copies into a 784-byte slot (the window starts 0 or 8
+// bytes into its first 16-byte chunk); lanes then read their node at a
+// 3-double stride (conflict-free for 64-bit shared loads).
+// Source arrays per row: APPLY/STATS: input; RESID: x, dinv; PCGA: r, p_old,
+// dinv, x; SHAPE: KB states.
+constexpr int kRowSlot = 98;  // doubles: 49 chunks of 16 bytes
+
 template <class PH, int ACT>
 struct Stage {
-  static constexpr int NR = (ACT == PCGA) ? 12 : (ACT == RESID) ? 6 : PH::NIN;
+  static constexpr int NS = (ACT == PCGA) ? 4 : (ACT == RESID) ? 2 : PH::NIN / 3;
   static constexpr int NOUT = PH::NOUT;
-  static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NR * 32;
+  static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NS * kRowSlot;
   static constexpr size_t words = (size_t)3 * (kWarps + 1) * 32;
   static constexpr size_t xchg = (size_t)2 * kWarps * 2 * NOUT * 32;  // double-buffered
   static constexpr size_t bytes = doubles * 8 + xchg * 8 + words * 4;
 };
 
+#ifndef LSG_M3_MINB
+#define LSG_M3_MINB 2
+#endif
+
 template <class PH, int ACT>
-__global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
+__global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, MArgs a) {
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
   constexpr int NP = Traits<ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
-  constexpr int NR = Stage<PH, ACT>::NR;
+  constexpr int NS = Stage<PH, ACT>::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *stage = reinterpret_cast<double *>(smem_raw);               // [3][kWarps+1][NR][32]
-  double *xchg = stage + Stage<PH, ACT>::doubles;                      // [kWarps][2*NOUT][32]
+  double *stage = reinterpret_cast<double *>(smem_raw);               // [3][kWarps+1][NS][kRowSlot]
+  double *xchg = stage + Stage<PH, ACT>::doubles;                      // [2][kWarps][2*NOUT][32]
   uint32_t *stw = reinterpret_cast<uint32_t *>(xchg + Stage<PH, ACT>::xchg);  // [3][kWarps+1][32]
   __shared__ double scratch[NPA * kWarps];
-  auto ST = [&](int slot, int row, int t, int l) -> double & {
-    return stage[(((size_t)slot * (kWarps + 1) + row) * NR + t) * 32 + l];
+  auto SR = [&](int slot, int row, int s) -> double * {
+    return stage + (((size_t)slot * (kWarps + 1) + row) * NS + s) * kRowSlot;
   };
   auto SW = [&](int slot, int row, int l) -> uint32_t & {
     return stw[((size_t)slot * (kWarps + 1) + row) * 32 + l];
@@ -117,6 +132,24 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
   const int kstart = max(K0 - 1, 0);
   const int kend = min(K1, nz);
 
+  // source arrays staged per row, and the 8-byte phase of each base pointer
+  const double *src[NS];
+  if constexpr (ACT == PCGA) {
+    src[0] = a.x + voff; src[1] = a.x2 + voff; src[2] = a.dinv; src[3] = a.xs + voff;
+  } else if constexpr (ACT == RESID) {
+    src[0] = a.x + voff; src[1] = a.dinv;
+  } else if constexpr (ACT == SHAPE) {
+#pragma unroll
+    for (int f = 0; f < NS; ++f) src[f] = a.x + (size_t)f * nn * 3;
+  } else {
+    src[0] = a.x + voff;
+  }
+  // column window of this strip: nodes lo..hi (clamped); lane reads node ic
+  const int lo = min(max((int)blockIdx.x * kStrip - 1, 0), nx);
+  const int hi = min(max((int)blockIdx.x * kStrip + kStrip, 0), nx);
+  const int li3 = (ic - lo) * 3;
+  const int wbytes = (hi - lo + 1) * 24;
+
   // stage plane kk of this warp's row (and, for the top warp, of the row above)
   auto issue = [&](int kk, int slot) {
     if (kk <= kend) {
@@ -124,25 +157,22 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
       for (int rr = 0; rr < nrows; ++rr) {
         const int row = rr == 0 ? jc : jxc;
         const int srow = w + rr;
-        const int64_t node = ((int64_t)kk * nyp + row) * nxp + ic;
-        cp_async4(&SW(slot, srow, lane), a.words + node);
-        const double *src[4];
-        int ns;
-        if constexpr (ACT == PCGA) {
-          src[0] = a.x + voff; src[1] = a.x2 + voff; src[2] = a.dinv; src[3] = a.xs + voff; ns = 4;
-        } else if constexpr (ACT == RESID) {
-          src[0] = a.x + voff; src[1] = a.dinv; ns = 2;
-        } else if constexpr (ACT == SHAPE) {
-          for (int f = 0; f < NIN / 3; ++f) src[f] = a.x + (size_t)f * nn * 3;
-          ns = NIN / 3;
-        } else {
-          src[0] = a.x + voff; ns = 1;
-        }
+        const int64_t n0 = ((int64_t)kk * nyp + row) * nxp + lo;
+        cp_async4(&SW(slot, srow, lane), a.words + n0 + (ic - lo));
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (s < ns) {
+        for (int s = 0; s < NS; ++s) {
+          const char *S = reinterpret_cast<const char *>(src[s] + n0 * 3);
+          const char *A = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(S) & ~(uintptr_t)15);
+          const char *E = S + wbytes;
+          char *dst = reinterpret_cast<char *>(SR(slot, srow, s));
 #pragma unroll
-            for (int q = 0; q < 3; ++q) cp_async8(&ST(slot, srow, 3 * s + q, lane), src[s] + node * 3 + q);
+          for (int c = lane; c < kRowSlot / 2; c += 32) {
+            const char *gp = A + 16 * c;
+            if (gp < E) {
+              if (gp < S) cp_async8(dst + 16 * c + 8, gp + 8);
+              else if (gp + 16 > E) cp_async8(dst + 16 * c, gp);
+              else cp_async16(dst + 16 * c, gp);
+            }
           }
         }
       }
@@ -151,27 +181,33 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
   };
 
   // operator input (masked), raw value, inverse diagonal of a staged row
-  auto prepare = [&](int kk, int slot, int srow, bool ok, bool write_own, double *in, double *raw,
-                     double *dg, uint32_t &wc) {
+  auto prepare = [&](int kk, int slot, int srow, int row, bool ok, bool write_own, double *in,
+                     double *raw, double *dg, uint32_t &wc) {
     wc = ok ? SW(slot, srow, lane) : 0u;
+    const int ph = (int)((((int64_t)kk * nyp + row) * nxp + lo) & 1);
+    auto V = [&](int s, int q) -> double {
+      const int off = ph ^ (int)((reinterpret_cast<uintptr_t>(src[s]) >> 3) & 1);
+      return SR(slot, srow, s)[off + li3 + q];
+    };
     if constexpr (ACT == SHAPE) {
 #pragma unroll
-      for (int t = 0; t < NIN; ++t) in[t] = ST(slot, srow, t, lane);
+      for (int t = 0; t < NIN; ++t) in[t] = V(t / 3, t % 3);
     } else {
       const uint32_t m = PH::mask(wc);
       double v[3];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) v[q] = ST(slot, srow, q, lane);
+      for (int q = 0; q < 3; ++q) v[q] = V(0, q);
       if constexpr (ACT == RESID) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) dg[q] = ST(slot, srow, 3 + q, lane);
+        for (int q = 0; q < 3; ++q) dg[q] = V(1, q);
       }
       if constexpr (ACT == PCGA) {
+        double po[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          dg[q] = ST(slot, srow, 6 + q, lane);
-          const double po = first ? 0.0 : ST(slot, srow, 3 + q, lane);
-          v[q] = fma(beta, po, v[q] * dg[q]);
+          dg[q] = V(2, q);
+          po[q] = V(1, q);
+          v[q] = fma(beta, first ? 0.0 : po[q], v[q] * dg[q]);
         }
         if (write_own) {
           const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
@@ -179,8 +215,7 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
           for (int q = 0; q < 3; ++q) {
             a.y2[voff + node * 3 + q] = v[q];
             if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
-              a.xs[voff + node * 3 + q] =
-                  fma(alpha_prev, ST(slot, srow, 3 + q, lane), ST(slot, srow, 9 + q, lane));
+              a.xs[voff + node * 3 + q] = fma(alpha_prev, po[q], V(3, q));
           }
         }
       }
@@ -251,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
     double raw_t[3], dg_t[3];
     uint32_t wt;
     const int s0 = kstart % 3;
-    prepare(kstart, s0, w, node_ok, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
-    prepare(kstart, s0, w + 1, up_ok, false, iy_c, raw_t, dg_t, wt);
+    prepare(kstart, s0, w, jc, node_ok, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
+    prepare(kstart, s0, w + 1, jxc, up_ok, false, iy_c, raw_t, dg_t, wt);
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
       rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
@@ -271,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 2) march3s(PH ph, Geo g, MArgs a) {
     const int sl = kk % 3;
     double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3], raw_t[3], dg_t[3];
     uint32_t wc_n, wt;
-    prepare(kk, sl, w, node_ok, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
-    prepare(kk, sl, w + 1, up_ok, false, iy_n, raw_t, dg_t, wt);
+    prepare(kk, sl, w, jc, node_ok, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
+    prepare(kk, sl, w + 1, jxc, up_ok, false, iy_n, raw_t, dg_t, wt);
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
       rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
