@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   const int kstart = max(K0 - 1, 0);
   const int kend = min(K1, nz);
 
-  // source arrays staged per row, and the 8-byte phase of each base pointer
+  // source arrays staged per row
   const double *src[NS];
   if constexpr (ACT == PCGA) {
     src[0] = a.x + voff; src[1] = a.x2 + voff; src[2] = a.dinv; src[3] = a.xs + voff;
@@ -144,50 +144,59 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   } else {
     src[0] = a.x + voff;
   }
+  // 8-byte phase of each base pointer: node n of array s starts at an odd
+  // multiple of 8 bytes iff bit s of spm differs from the parity of n
+  uint32_t spm = 0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) spm |= (uint32_t)((reinterpret_cast<uintptr_t>(src[s]) >> 3) & 1u) << s;
   // column window of this strip: nodes lo..hi (clamped); lane reads node ic
   const int lo = min(max((int)blockIdx.x * kStrip - 1, 0), nx);
   const int hi = min(max((int)blockIdx.x * kStrip + kStrip, 0), nx);
   const int li3 = (ic - lo) * 3;
   const int wbytes = (hi - lo + 1) * 24;
+  const int64_t rown = (int64_t)jc * nxp + lo, rowu = (int64_t)jxc * nxp + lo;
 
-  // stage plane kk of this warp's row (and, for the top warp, of the row above)
-  auto issue = [&](int kk, int slot) {
-    if (kk <= kend) {
-      const int nrows = top ? 2 : 1;
-      for (int rr = 0; rr < nrows; ++rr) {
-        const int row = rr == 0 ? jc : jxc;
-        const int srow = w + rr;
-        const int64_t n0 = ((int64_t)kk * nyp + row) * nxp + lo;
-        cp_async4(&SW(slot, srow, lane), a.words + n0 + (ic - lo));
+  // stage the window of node row n0.. (one plane) into ring slot `slot`
+  auto stage_row = [&](int64_t n0, int slot, int srow) {
+    cp_async4(&SW(slot, srow, lane), a.words + n0 + (ic - lo));
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const char *S = reinterpret_cast<const char *>(src[s] + n0 * 3);
-          const char *A = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(S) & ~(uintptr_t)15);
-          const char *E = S + wbytes;
-          char *dst = reinterpret_cast<char *>(SR(slot, srow, s));
-#pragma unroll
-          for (int c = lane; c < kRowSlot / 2; c += 32) {
-            const char *gp = A + 16 * c;
-            if (gp < E) {
-              if (gp < S) cp_async8(dst + 16 * c + 8, gp + 8);
-              else if (gp + 16 > E) cp_async8(dst + 16 * c, gp);
-              else cp_async16(dst + 16 * c, gp);
-            }
+    for (int s = 0; s < NS; ++s) {
+      const char *S = reinterpret_cast<const char *>(src[s] + n0 * 3);
+      const char *A = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(S) & ~(uintptr_t)15);
+      char *dst = reinterpret_cast<char *>(SR(slot, srow, s));
+      if (A + 16 * (kRowSlot / 2) <= reinterpret_cast<const char *>(src[s] + nn * 3)) {
+        // 49 chunks cover the window whatever its phase (it may over-read
+        // up to 16 bytes past the window, never past the array)
+        cp_async16(dst + 16 * lane, A + 16 * lane);
+        if (lane < kRowSlot / 2 - 32) cp_async16(dst + 512 + 16 * lane, A + 512 + 16 * lane);
+      } else {  // the array's last row: exact chunks
+        const char *E = S + wbytes;
+        for (int c = lane; c < kRowSlot / 2; c += 32) {
+          const char *gp = A + 16 * c;
+          if (gp < E) {
+            if (gp < S) cp_async8(dst + 16 * c + 8, gp + 8);
+            else if (gp + 16 > E) cp_async8(dst + 16 * c, gp);
+            else cp_async16(dst + 16 * c, gp);
           }
         }
       }
+    }
+  };
+  auto issue = [&](int kk, int slot) {
+    if (kk <= kend) {
+      stage_row(kk * plane + rown, slot, w);
+      if (top) stage_row(kk * plane + rowu, slot, w + 1);
     }
     cp_async_commit();
   };
 
   // operator input (masked), raw value, inverse diagonal of a staged row
-  auto prepare = [&](int kk, int slot, int srow, int row, bool ok, bool write_own, double *in,
+  auto prepare = [&](int kk, int slot, int srow, int64_t rowoff, bool ok, bool write_own, double *in,
                      double *raw, double *dg, uint32_t &wc) {
     wc = ok ? SW(slot, srow, lane) : 0u;
-    const int ph = (int)((((int64_t)kk * nyp + row) * nxp + lo) & 1);
+    const uint32_t ph = (uint32_t)((kk * plane + rowoff) & 1);
     auto V = [&](int s, int q) -> double {
-      const int off = ph ^ (int)((reinterpret_cast<uintptr_t>(src[s]) >> 3) & 1);
-      return SR(slot, srow, s)[off + li3 + q];
+      return SR(slot, srow, s)[(int)(ph ^ ((spm >> s) & 1u)) + li3 + q];
     };
     if constexpr (ACT == SHAPE) {
 #pragma unroll
@@ -202,12 +211,13 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
         for (int q = 0; q < 3; ++q) dg[q] = V(1, q);
       }
       if constexpr (ACT == PCGA) {
+        // p = D^-1 r + beta p_old (p_old is zeroed by pcg_start, beta = 0 first)
         double po[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           dg[q] = V(2, q);
           po[q] = V(1, q);
-          v[q] = fma(beta, first ? 0.0 : po[q], v[q] * dg[q]);
+          v[q] = fma(beta, po[q], v[q] * dg[q]);
         }
         if (write_own) {
           const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
@@ -275,65 +285,52 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     }
   };
 
-  double in_c[NIN], rt_c[NIN], iy_c[NIN], iyr_c[NIN], raw_c[3], dg_c[3], acc[NOUT];
-  uint32_t wc_c;
-  issue(kstart, kstart % 3);
-  issue(kstart + 1, (kstart + 1) % 3);
-  {
-    cp_async_wait<1>();
-    __syncthreads();
-    issue(kstart + 2, (kstart + 2) % 3);
+  // Marching state of one plane: own-row input, its x-neighbour (lane+1),
+  // the row above and its x-neighbour; raw values / inverse diagonal / word
+  // for the emission of this plane's node.
+  struct PlaneState {
+    double in[NIN], rt[NIN], iy[NIN], iyr[NIN], raw[3], dg[3];
+    uint32_t wc;
+  };
+  auto load_plane = [&](int kk, int slot, bool write_own, PlaneState &s) {
     double raw_t[3], dg_t[3];
     uint32_t wt;
-    const int s0 = kstart % 3;
-    prepare(kstart, s0, w, jc, node_ok, own && kstart >= K0, in_c, raw_c, dg_c, wc_c);
-    prepare(kstart, s0, w + 1, jxc, up_ok, false, iy_c, raw_t, dg_t, wt);
+    prepare(kk, slot, w, rown, node_ok, write_own, s.in, s.raw, s.dg, s.wc);
+    prepare(kk, slot, w + 1, rowu, up_ok, false, s.iy, raw_t, dg_t, wt);
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
-      rt_c[t] = __shfl_down_sync(0xffffffffu, in_c[t], 1);
-      iyr_c[t] = __shfl_down_sync(0xffffffffu, iy_c[t], 1);
+      s.rt[t] = __shfl_down_sync(0xffffffffu, s.in[t], 1);
+      s.iyr[t] = __shfl_down_sync(0xffffffffu, s.iy[t], 1);
     }
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) acc[t] = 0.0;
-    cp_async_wait<1>();  // plane kstart+1 has landed
-    __syncthreads();     // ... for every thread
-  }
+  };
+  const int wm1 = w > 0 ? w - 1 : 0;  // warp 0 (halo row, never emits) reads its own slot
 
-  // One barrier per plane: it publishes both this step's y-contributions
-  // (exchange buffer double-buffered by parity) and the staged plane kk+1.
-  for (int kk = kstart + 1; kk <= kend; ++kk) {
-    issue(kk + 2, (kk + 2) % 3);  // slot of plane kk-1, fully read before the last barrier
-    const int sl = kk % 3;
-    double in_n[NIN], rt_n[NIN], iy_n[NIN], iyr_n[NIN], raw_n[3], dg_n[3], raw_t[3], dg_t[3];
-    uint32_t wc_n, wt;
-    prepare(kk, sl, w, jc, node_ok, own && kk >= K0 && kk < K1, in_n, raw_n, dg_n, wc_n);
-    prepare(kk, sl, w + 1, jxc, up_ok, false, iy_n, raw_t, dg_t, wt);
-#pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      rt_n[t] = __shfl_down_sync(0xffffffffu, in_n[t], 1);
-      iyr_n[t] = __shfl_down_sync(0xffffffffu, iy_n[t], 1);
-    }
+  // One step: cells (., ., kk-1) from planes kk-1 (c) and kk (n); emits plane
+  // kk-1.  Lane 0 and warp 0 are halo: their sums are never emitted, so the
+  // shuffle / exchange edges need no zero-fill.  One barrier per plane: it
+  // publishes this step's y-contributions (exchange double-buffered by
+  // parity) and the staged plane kk+1.
+  auto step = [&](int kk, int sl, int sl2, PlaneState &c, PlaneState &n, double *acc_c,
+                  double *acc_n) {
+    issue(kk + 2, sl2);  // slot of plane kk-1, fully read before the last barrier
+    load_plane(kk, sl, own && kk >= K0 && kk < K1, n);
     double U[8][NIN];
 #pragma unroll
     for (int t = 0; t < NIN; ++t) {
-      U[0][t] = in_c[t];  U[1][t] = rt_c[t];  U[2][t] = iy_c[t];  U[3][t] = iyr_c[t];
-      U[4][t] = in_n[t];  U[5][t] = rt_n[t];  U[6][t] = iy_n[t];  U[7][t] = iyr_n[t];
+      U[0][t] = c.in[t];  U[1][t] = c.rt[t];  U[2][t] = c.iy[t];  U[3][t] = c.iyr[t];
+      U[4][t] = n.in[t];  U[5][t] = n.rt[t];  U[6][t] = n.iy[t];  U[7][t] = n.iyr[t];
     }
     double C[8][NOUT];
     if constexpr (ACT == SHAPE) {
-      ph.cell(U, wc_c, own && (kk - 1) >= K0, C, part);
+      ph.cell(U, c.wc, own && (kk - 1) >= K0, C, part);
     } else {
-      ph.cell(U, wc_c, i, jw, kk - 1, C);
+      ph.cell(U, c.wc, i, jw, kk - 1, C);
     }
     double T[4][NOUT];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int t = 0; t < NOUT; ++t) {
-        double up = __shfl_up_sync(0xffffffffu, C[2 * q + 1][t], 1);
-        if (lane == 0) up = 0.0;
-        T[q][t] = C[2 * q][t] + up;
-      }
+      for (int t = 0; t < NOUT; ++t) T[q][t] = C[2 * q][t] + __shfl_up_sync(0xffffffffu, C[2 * q + 1][t], 1);
     const int par = kk & 1;
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) {
@@ -342,27 +339,44 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     }
     cp_async_wait<1>();  // plane kk+1 has landed (kk+2 may still be in flight)
     __syncthreads();
-    double nxt[NOUT];
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) {
-      const double b0 = w > 0 ? SC(par, w - 1, t, lane) : 0.0;
-      const double b1 = w > 0 ? SC(par, w - 1, NOUT + t, lane) : 0.0;
-      acc[t] += T[0][t] + b0;
-      nxt[t] = T[2][t] + b1;
+      acc_c[t] += T[0][t] + SC(par, wm1, t, lane);
+      acc_n[t] = T[2][t] + SC(par, wm1, NOUT + t, lane);
     }
-    if (own && (kk - 1) >= K0) emit(kk - 1, wc_c, acc, raw_c, dg_c);
+    if (own && (kk - 1) >= K0) emit(kk - 1, c.wc, acc_c, c.raw, c.dg);
+  };
+
+  PlaneState P0, P1;
+  double acc0[NOUT], acc1[NOUT];
+  auto nxt3 = [](int s) { return s == 2 ? 0 : s + 1; };
+  int sl = kstart % 3;
+  issue(kstart, sl);
+  issue(kstart + 1, nxt3(sl));
+  cp_async_wait<1>();
+  __syncthreads();
+  issue(kstart + 2, nxt3(nxt3(sl)));
+  load_plane(kstart, sl, own && kstart >= K0, P0);
 #pragma unroll
-    for (int t = 0; t < NIN; ++t) {
-      in_c[t] = in_n[t]; rt_c[t] = rt_n[t]; iy_c[t] = iy_n[t]; iyr_c[t] = iyr_n[t];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { raw_c[q] = raw_n[q]; dg_c[q] = dg_n[q]; }
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) acc[t] = nxt[t];
-    wc_c = wc_n;
+  for (int t = 0; t < NOUT; ++t) acc0[t] = 0.0;
+  cp_async_wait<1>();  // plane kstart+1 has landed
+  __syncthreads();     // ... for every thread
+
+  // two steps per trip with the roles of the plane states swapped: no
+  // register copies between steps
+  bool last_in_1 = false;
+  for (int kk = kstart + 1; kk <= kend; kk += 2) {
+    sl = nxt3(sl);  // slot of plane kk
+    step(kk, sl, nxt3(nxt3(sl)), P0, P1, acc0, acc1);
+    if (kk == kend) { last_in_1 = true; break; }
+    sl = nxt3(sl);
+    step(kk + 1, sl, nxt3(nxt3(sl)), P1, P0, acc1, acc0);
   }
   cp_async_wait<0>();
-  if (K1 == nz + 1 && own && nz >= K0) emit(nz, wc_c, acc, raw_c, dg_c);
+  if (K1 == nz + 1 && own && nz >= K0) {  // plane nz: the last state written
+    if (last_in_1) emit(nz, P1.wc, acc1, P1.raw, P1.dg);
+    else emit(nz, P0.wc, acc0, P0.raw, P0.dg);
+  }
 
   if constexpr (NP > 0) {
     const int nblk = gridDim.x * gridDim.y * nzseg;

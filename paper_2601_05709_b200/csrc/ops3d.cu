@@ -874,6 +874,9 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   a.counters = ws.counters;
   rc = dispatch<RESID>(op, a, ws.k, st);
   if (rc) return rc;
+  // the first pass A reads p_old = ws.p with beta = 0: it must be finite
+  if (cudaMemsetAsync(ws.p, 0, sizeof(double) * (size_t)n * ws.k, st) != cudaSuccess)
+    return check_launch("pcg_start3d memset");
   zero_if_flag<<<dim3(64, ws.k), 256, 0, st>>>(n, ws.scal, ws.x);
   return check_launch("zero_if_flag3d");
 }
