@@ -61,6 +61,11 @@ typedef struct {
  *                 aux[2] = previous iterate (lsg_pg_reinit_rhs only). */
 #define LSG_OP_PG_TRANSPORT 3
 #define LSG_OP_PG_REINIT 4
+/* Scalar diffusion (a grad u, grad v) with the two-phase conductivity of the
+ * heat models (models/heat.py:113-119, fem.py:388-394), 2D only as the
+ * reference: words = lsg_material words (bit 5 = Dirichlet node),
+ * p0 = outside (contrast, heat.py:34), p1 = inside conductivity. */
+#define LSG_OP_LAPLACE 5
 
 /* Matrix-free operator description.
  *   ELASTICITY: words = per-node material word written by lsg_material
@@ -200,6 +205,19 @@ int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream);
 int lsg_shape_rhs(const lsg_op *op, int32_t k, const double *u, double volume,
                   double *vec_cost, double *vec_vol, double *out, double *s1,
                   double *partials, uint32_t *counter, void *stream);
+
+/* Thermal compliance and its shape derivative for k heat terms in one pass
+ * (replaces HeatModel.cost / constraint / derivative, models/heat.py:124-166,
+ * and the S0/S1 contraction of velocity.py:129-142).  op = LSG_OP_LAPLACE;
+ * u = k temperature fields (k, N); weights = k host doubles (term weights);
+ * fq = source samples at the quadrature points (k, E, 3) (device);
+ * gq = source gradients (k, E, 3, 2) or NULL (S0 = 0).  Writes vec_cost and
+ * vec_vol (2N each, velocity space) and out[0] = J, out[1] = subzero volume;
+ * partials/counter as for lsg_shape_rhs. */
+int lsg_heat_shape(const lsg_op *op, int32_t k, const double *u, const double *weights,
+                   const double *fq, const double *gq, double volume, double *vec_cost,
+                   double *vec_vol, double *out, double *partials, uint32_t *counter,
+                   void *stream);
 
 /* S1 of the cost per element and quadrature point, (E, nq, dim, dim), for
  * parity with ComplianceModel.derivative's tensor (compliance.py:128-139):

@@ -14,7 +14,13 @@ Restates, dimension-generically:
   (+ boundary-normal penalty, + frozen mass, + zero Dirichlet), RHS
   vec_a = int S0 . N_a + S1 : grad(N_a e_c), theta = B^-1 (-vec),
   form_value = theta^T B theta, derivative = vec . theta;
-* PPL recursion and Lagrangian (``ppl.py:47-63,100-114``).
+* PPL recursion and Lagrangian (``ppl.py:47-63,100-114``);
+* ``HeatModel`` / ``HeatPlusModel`` (``models/heat.py:78-171``): two-phase
+  conductivity A_q (contrast 1e-3, ``:34,113-114``), one grounded solve per
+  term (``:59-76,116-122``), adjoint -c_t u_t (``:124-128``),
+  J = sum_t c_t int A |grad u_t|^2 (``:130-138``), S0 = sum_t c_t 2 u grad f,
+  S1 = sum_t c_t ((2 u f - A |grad u|^2) I + 2 A grad u (x) grad u)
+  (``:143-166``).
 """
 
 from dataclasses import dataclass, replace
@@ -99,6 +105,79 @@ class Compliance:
 
     def s1_combined(self, phi, states, lam):
         return self.s1_cost(phi, states) + lam * self.s1_volume(phi)
+
+
+class Heat:
+    """Summed thermal compliance with a volume constraint (reference ``models/heat.py``).
+
+    ``terms`` = [(weight, ground node list, f_q (E, 3), gradf_q (E, 3, 2) or None)];
+    a None weight means 1 / len(terms) (``heat.py:107-111``).
+    """
+
+    CONTRAST = 1e-3
+
+    def __init__(self, grid, terms, volume, contrast=CONTRAST):
+        self.grid = grid
+        self.space = fem.Space(grid, 1)
+        self.contrast = float(contrast)
+        self.volume = float(volume)
+        default_w = 1.0 / len(terms)
+        self.terms = []
+        for w, ground, f_q, g_q in terms:
+            load = self.space.assemble_vector(
+                np.einsum("tq,qa->ta", self.space.quad_weights * f_q, self.space.bary))
+            self.terms.append((default_w if w is None else float(w), np.asarray(ground, dtype=np.int64),
+                               np.asarray(f_q, dtype=float), None if g_q is None else np.asarray(g_q, dtype=float),
+                               load))
+
+    def chi(self, phi):
+        return fem.phi_at_quad_sign(self.space, phi).astype(float)
+
+    def a_q(self, phi):
+        chi = self.chi(phi)
+        return chi + self.contrast * (1.0 - chi)
+
+    def matrix(self, phi):
+        return self.space.assemble_matrix(fem.stiffness_elements(self.space, self.a_q(phi)))
+
+    def solve_states(self, phi, rtol=fem.CG_RTOL):
+        K = self.matrix(phi)
+        states, iters = [], []
+        for _, ground, _, _, load in self.terms:
+            A, b = fem.dirichlet_eliminate(K, load, ground)
+            x, it = fem.jacobi_pcg(A, b, rtol=rtol)
+            states.append(x)
+            iters.append(it)
+        return states, iters
+
+    def cost(self, phi, states):
+        a_q = self.a_q(phi)
+        total = 0.0
+        for (w, *_), u in zip(self.terms, states):
+            g = self.space.grad_at_quad(u)
+            dens = np.einsum("td,td->t", g, g)
+            total += w * float(np.sum(self.space.quad_weights * (a_q * dens[:, None])))
+        return total
+
+    def constraint(self, phi):
+        return float(np.sum(self.space.quad_weights * self.chi(phi))) / self.volume
+
+    def tensors(self, phi, states):
+        """(S0, S1) of the cost at the quadrature points (``heat.py:143-166``)."""
+        a_q = self.a_q(phi)
+        nt, nq = a_q.shape
+        s0 = np.zeros((nt, nq, 2))
+        s1 = np.zeros((nt, nq, 2, 2))
+        for (w, _, f_q, g_q, _), u in zip(self.terms, states):
+            u_q = np.einsum("qa,ta->tq", self.space.bary, u[self.grid.elements])
+            g = self.space.grad_at_quad(u)
+            dens = np.einsum("td,td->t", g, g)
+            if g_q is not None:
+                s0 += w * 2.0 * u_q[:, :, None] * g_q
+            scal = 2.0 * u_q * f_q - a_q * dens[:, None]
+            outer = np.einsum("ti,tj->tij", g, g)
+            s1 += w * (scal[:, :, None, None] * np.eye(2) + 2.0 * a_q[:, :, None, None] * outer[:, None, :, :])
+        return s0, s1
 
 
 def derivative_vector(space, s1=None, s0=None):

@@ -13,12 +13,12 @@ operation raises.
 from .driver import (IterationRecord, RunParams, adaptive_time, run, solve_concurrent,
                      stopping_check)
 from .errors import ConfigError, NewtonError, SolverError
-from .fem import (DirichletSet, ElasticityOperator, FemField, FunctionSpace, H1Operator,
+from .fem import (DirichletSet, ElasticityOperator, FemField, FunctionSpace, H1Operator, LaplaceOperator,
                   LinearProblem, solve_batched, solve_linear)
 from .levelset import InitialLevelSpec, LevelSetField, initial_level, reinitialize, transport
 from .mesh import (BoxMesh, RectMesh, build_box_mesh, build_rect_mesh, mesh_diameter,
                    tag_boundary)
-from .models import ComplianceModel, CompliancePlusModel
+from .models import ComplianceModel, CompliancePlusModel, HeatModel, HeatPlusModel, HeatTerm
 from .ppl import combine_derivatives, lagrangian_value, ppl_init, ppl_update
 from .velocity import BilinearSpec, DerivativePair, VelocityResult, VelocitySolver
 
@@ -27,8 +27,8 @@ __all__ = [
     "stopping_check", "solve_concurrent", "run", "RectMesh", "BoxMesh", "build_rect_mesh",
     "build_box_mesh", "mesh_diameter", "tag_boundary", "InitialLevelSpec", "LevelSetField",
     "initial_level", "reinitialize", "transport", "FunctionSpace", "FemField", "DirichletSet",
-    "ElasticityOperator", "H1Operator", "LinearProblem", "solve_linear", "solve_batched",
-    "ComplianceModel", "CompliancePlusModel", "BilinearSpec", "DerivativePair", "VelocityResult",
+    "ElasticityOperator", "H1Operator", "LaplaceOperator", "LinearProblem", "solve_linear", "solve_batched",
+    "ComplianceModel", "CompliancePlusModel", "HeatModel", "HeatPlusModel", "HeatTerm", "BilinearSpec", "DerivativePair", "VelocityResult",
     "VelocitySolver", "combine_derivatives", "lagrangian_value", "ppl_init", "ppl_update",
 ]
 

@@ -23,6 +23,7 @@ LSG_OP_ELASTICITY = 1
 LSG_OP_H1 = 2
 LSG_OP_PG_TRANSPORT = 3
 LSG_OP_PG_REINIT = 4
+LSG_OP_LAPLACE = 5
 
 SCAL_FIELDS = ("atol", "rho", "alpha", "beta", "rr", "pq", "bb", "iters", "done", "zero_rhs",
                "maxiter", "first", "rz_new")
@@ -79,6 +80,7 @@ SIGNATURES = {
     "lsg_pcg_iterate": (ctypes.c_int, [_O, _W, _I, _P]),
     "lsg_pcg_finish": (ctypes.c_int, [_O, _W, _P]),
     "lsg_shape_rhs": (ctypes.c_int, [_O, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P]),
+    "lsg_heat_shape": (ctypes.c_int, [_O, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
     "lsg_s1_tensor": (ctypes.c_int, [_O, _I, _P, _P, _P, _P]),
     "lsg_tensor_rhs": (ctypes.c_int, [_G, _P, _P, _P, _P]),
     "lsg_velocity_rhs": (ctypes.c_int, [_O, _P, _P, _D, _P, _P]),

@@ -56,7 +56,11 @@ static int check_op(const lsg_op *op) {
     if (!(op->p[0] > 0.0) || !(op->p[1] > 0.0)) { set_error("PG operator needs dt > 0 and h > 0"); return LSG_ERR_ARG; }
     return LSG_OK;
   }
-  if (op->kind != LSG_OP_ELASTICITY && op->kind != LSG_OP_H1) {
+  if (op->kind == LSG_OP_LAPLACE && op->grid.dim != 2) {
+    set_error("the scalar diffusion operator (heat models) is 2D only, as the reference");
+    return LSG_ERR_ARG;
+  }
+  if (op->kind != LSG_OP_ELASTICITY && op->kind != LSG_OP_H1 && op->kind != LSG_OP_LAPLACE) {
     set_error("unknown operator kind %d", op->kind);
     return LSG_ERR_ARG;
   }
@@ -231,6 +235,19 @@ int lsg_shape_rhs(const lsg_op *op, int32_t k, const double *u, double volume, d
   return DISPATCH(op->grid,
                   shape_rhs(*op, k, u, volume, vec_cost, vec_vol, out, partials, counter, S(stream)),
                   shape_rhs(*op, k, u, volume, vec_cost, vec_vol, out, partials, counter, S(stream)));
+}
+
+int lsg_heat_shape(const lsg_op *op, int32_t k, const double *u, const double *weights,
+                   const double *fq, const double *gq, double volume, double *vec_cost,
+                   double *vec_vol, double *out, double *partials, uint32_t *counter,
+                   void *stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  if (op->kind != LSG_OP_LAPLACE) { set_error("heat_shape needs the scalar diffusion operator"); return LSG_ERR_ARG; }
+  if (k < 1 || !weights || !fq || !u) { set_error("heat_shape needs k >= 1 states, weights and source samples"); return LSG_ERR_ARG; }
+  if (!(volume > 0.0)) { set_error("target volume must be positive"); return LSG_ERR_ARG; }
+  return d2::heat_shape(*op, k, u, weights, fq, gq, volume, vec_cost, vec_vol, out, partials,
+                        counter, S(stream));
 }
 
 int lsg_s1_tensor(const lsg_op *op, int32_t k, const double *u, const double *phi, double *s1,

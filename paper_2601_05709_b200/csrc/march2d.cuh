@@ -37,6 +37,34 @@ struct Geo {
   double hx, hy;
 };
 
+// Node vectors of NC interleaved components (2: displacement / velocity,
+// 1: temperature): one 16-byte or 8-byte access per node.
+template <int NC>
+__device__ __forceinline__ void ldg_node(const double *base, int64_t node, double *v) {
+  if constexpr (NC == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2 *>(base) + node);
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    v[0] = __ldg(base + node);
+  }
+}
+template <int NC>
+__device__ __forceinline__ void ld_node(const double *base, int64_t node, double *v) {
+  if constexpr (NC == 2) {
+    const double2 t = reinterpret_cast<const double2 *>(base)[node];
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    v[0] = base[node];
+  }
+}
+template <int NC>
+__device__ __forceinline__ void st_node(double *base, int64_t node, const double *v) {
+  if constexpr (NC == 2) reinterpret_cast<double2 *>(base)[node] = make_double2(v[0], v[1]);
+  else base[node] = v[0];
+}
+
 // ---------------------------------------------------------------------------
 // Elasticity (fem.py:397-411).  Word (uint8, written by lsg_material):
 //   bits 0-1 n_in of the lower triangle, bits 2-3 n_in of the upper triangle
@@ -51,7 +79,7 @@ struct Geo {
 // lower: r_a = -A, r_b = A - B, r_c = B ; upper: r_a = -B, r_c = A, r_d = B - A.
 // ---------------------------------------------------------------------------
 struct Elast {
-  static constexpr int NIN = 2, NOUT = 2;
+  static constexpr int NC = 2, NIN = 2, NOUT = 2;
   double k1, k2, k3, k4, k5, k6;
   double w0, w1;  // w(n_in) = w0 + w1 * n_in = |T| (n_in + (3 - n_in) ersatz) / 3
 
@@ -99,6 +127,45 @@ struct Elast {
 };
 
 // ---------------------------------------------------------------------------
+// Scalar diffusion (a grad u, grad v) with the ersatz conductivity of the heat
+// models (models/heat.py:113-119, fem.py:388-394).  Same material word as
+// Elast (bit 5 = Dirichlet on the node).  With dP = u(right) - u(left),
+// dQ = u(top) - u(bottom) the fluxes are X = w dP / hx^2, Y = w dQ / hy^2:
+// lower r_a = -X, r_b = X - Y, r_c = Y ; upper r_a = -Y, r_c = X, r_d = Y - X.
+// ---------------------------------------------------------------------------
+struct Lap {
+  static constexpr int NC = 1, NIN = 1, NOUT = 1;
+  double w0, w1;      // |T| abar(n_in) = w0 + w1 n_in
+  double ihx2, ihy2;  // 1 / hx^2, 1 / hy^2
+
+  __device__ __forceinline__ double wof(uint32_t n) const { return fma((double)n, w1, w0); }
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 4) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t w) { return (w >> 5) & 1u; }
+
+  __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
+                                       const double *u11, uint32_t word, int, int, double *c00,
+                                       double *c10, double *c01, double *c11) const {
+    const double v = valid(word) ? 1.0 : 0.0;
+    const double wl = wof(word & 3u) * v, wu = wof((word >> 2) & 3u) * v;
+    const double XL = wl * ihx2 * (u10[0] - u00[0]), YL = wl * ihy2 * (u11[0] - u10[0]);
+    const double XU = wu * ihx2 * (u11[0] - u01[0]), YU = wu * ihy2 * (u01[0] - u00[0]);
+    c00[0] = -XL - YU;
+    c10[0] = XL - YL;
+    c11[0] = YL + XU;
+    c01[0] = YU - XU;
+  }
+
+  // sum_e w_e |grad N|^2 over the six triangles around the node
+  __device__ __forceinline__ void diag(uint32_t w00, uint32_t wm0, uint32_t w0m, uint32_t wmm,
+                                       double *d) const {
+    auto wl = [&](uint32_t w) { return valid(w) ? wof(w & 3u) : 0.0; };
+    auto wu = [&](uint32_t w) { return valid(w) ? wof((w >> 2) & 3u) : 0.0; };
+    d[0] = (wl(w00) + wu(wmm)) * ihx2 + (wu(w00) + wl(wmm)) * ihy2 +
+           (wl(wm0) + wu(w0m)) * (ihx2 + ihy2);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // H1 velocity form (velocity.py:98-127), componentwise:
 //   B = mw M + sw K_lap + fp M_frozen + np * boundary normal mass.
 // Word (uint8, lsg_h1_words): bits 0-2 frozen flags of the lower triangle's
@@ -106,7 +173,7 @@ struct Elast {
 // bit 6 Dirichlet (both components), bit 7 cell valid.
 // ---------------------------------------------------------------------------
 struct H1 {
-  static constexpr int NIN = 2, NOUT = 2;
+  static constexpr int NC = 2, NIN = 2, NOUT = 2;
   int nx, ny;
   double m;       // mw * |T| / 12
   double ax, ay;  // sw * |T| / hx^2, sw * |T| / hy^2

@@ -34,7 +34,7 @@ struct MArgs {
 // in = KB displacement fields, out = (vec_cost[2], vec_vol[2]).
 template <int KB>
 struct Shape {
-  static constexpr int NIN = 2 * KB, NOUT = 4;
+  static constexpr int NC = 2, NIN = 2 * KB, NOUT = 4;
   double lam, mu, area, inv_hx, inv_hy, inv_volume;
   double w0, w1;  // |T| * abar(n_in) = w0 + w1 n_in
 
@@ -64,8 +64,9 @@ struct Shape {
   }
 
   __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
-                                       const double *u11, uint32_t word, bool count, double *c00,
-                                       double *c10, double *c01, double *c11, double *part) const {
+                                       const double *u11, uint32_t word, bool count, int, int,
+                                       double *c00, double *c10, double *c01, double *c11,
+                                       double *part) const {
     const bool ok = valid(word);
     const uint32_t nl = ok ? (word & 3u) : 0u, nu = ok ? ((word >> 2) & 3u) : 0u;
     const double wl = ok ? fma((double)nl, w1, w0) : 0.0, wu = ok ? fma((double)nu, w1, w0) : 0.0;
@@ -99,6 +100,122 @@ struct Shape {
   }
 };
 
+// Thermal compliance + shape derivative for KB heat terms at once
+// (models/heat.py:124-166): per term t with weight c_t, state u_t, source
+// samples f_q (and optionally grad f_q) at the three edge-midpoint points,
+//   J   += c_t int A |grad u|^2,
+//   S1_q = c_t ((2 u_q f_q - A_q |grad u|^2) I + 2 A_q grad u (x) grad u),
+//   S0_q = c_t 2 u_q grad f_q,
+// contracted with the test functions: vec_a += sum_q (|T|/3) (S0_q N_a(x_q)
+// + S1_q grad N_a).  grad u is constant per triangle, so only sum_q A_q =
+// 3 abar enters the S1 term.  in = KB temperature fields; out =
+// (vec_cost[2], vec_vol[2]) as for Shape.
+template <int KB>
+struct HeatShape {
+  static constexpr int NC = 1, NIN = KB, NOUT = 4;
+  int nx;
+  double area, inv_hx, inv_hy, inv_volume;
+  double w0, w1;        // |T| abar(n_in) = w0 + w1 n_in
+  double cw[KB];        // term weights
+  const double *fq;     // (KB, E, 3) source samples
+  const double *gq;     // (KB, E, 3, 2) source gradients, or null
+  int64_t ecount;       // number of triangles E (stride of one term in fq / gq)
+  __device__ __forceinline__ int64_t estride() const { return ecount; }
+
+  __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 4) & 1u; }
+  __device__ __forceinline__ static uint32_t mask(uint32_t) { return 0u; }
+
+  __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
+                                       const double *u11, uint32_t word, bool count, int i, int j,
+                                       double *c00, double *c10, double *c01, double *c11,
+                                       double *part) const {
+    const bool ok = valid(word);
+    const uint32_t nl = ok ? (word & 3u) : 0u, nu = ok ? ((word >> 2) & 3u) : 0u;
+    const double wl = ok ? fma((double)nl, w1, w0) : 0.0, wu = ok ? fma((double)nu, w1, w0) : 0.0;
+    const double qw = ok ? area * (1.0 / 3.0) : 0.0;  // quadrature weight (0 off the grid)
+    // element indices (fem order: lower 2c, upper 2c+1); clamp halo cells to a valid index
+    const int64_t cidx = ok ? ((int64_t)j * nx + i) : 0;
+    const int64_t el = 2 * cidx, eu = el + 1;
+    double Mxx = 0.0, Mxy = 0.0, Myy = 0.0, Nxx = 0.0, Nxy = 0.0, Nyy = 0.0, dens = 0.0;
+    // S0 vertex sums: lower (00, 10, 11), upper (00, 11, 01)
+    double sL[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double sU[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const double c = cw[k];
+      const double *f = fq + (size_t)k * (size_t)estride() * 3;
+      // lower: grad u = ((u10 - u00)/hx, (u11 - u10)/hy)
+      {
+        const double gx = (u10[k] - u00[k]) * inv_hx, gy = (u11[k] - u10[k]) * inv_hy;
+        const double q0 = 0.5 * (u00[k] + u10[k]), q1 = 0.5 * (u10[k] + u11[k]),
+                     q2 = 0.5 * (u00[k] + u11[k]);
+        const double uf = q0 * f[el * 3] + q1 * f[el * 3 + 1] + q2 * f[el * 3 + 2];
+        const double g2 = gx * gx + gy * gy;
+        const double diag = 2.0 * qw * uf - wl * g2;
+        Mxx += c * (diag + 2.0 * wl * gx * gx);
+        Myy += c * (diag + 2.0 * wl * gy * gy);
+        Mxy += c * (2.0 * wl * gx * gy);
+        dens += c * wl * g2;
+        if (gq) {
+          const double *G = gq + (size_t)k * (size_t)estride() * 6 + el * 6;
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const double t0 = c * qw * q0 * G[d], t1 = c * qw * q1 * G[2 + d], t2 = c * qw * q2 * G[4 + d];
+            sL[0][d] += t0 + t2;  // vertex A in edges (A,B), (A,C)
+            sL[1][d] += t0 + t1;  // vertex B in (A,B), (B,C)
+            sL[2][d] += t1 + t2;  // vertex C in (B,C), (A,C)
+          }
+        }
+      }
+      // upper (A, B, C) = (00, 11, 01): grad u = ((u11 - u01)/hx, (u01 - u00)/hy)
+      {
+        const double gx = (u11[k] - u01[k]) * inv_hx, gy = (u01[k] - u00[k]) * inv_hy;
+        const double q0 = 0.5 * (u00[k] + u11[k]), q1 = 0.5 * (u11[k] + u01[k]),
+                     q2 = 0.5 * (u00[k] + u01[k]);
+        const double uf = q0 * f[eu * 3] + q1 * f[eu * 3 + 1] + q2 * f[eu * 3 + 2];
+        const double g2 = gx * gx + gy * gy;
+        const double diag = 2.0 * qw * uf - wu * g2;
+        Nxx += c * (diag + 2.0 * wu * gx * gx);
+        Nyy += c * (diag + 2.0 * wu * gy * gy);
+        Nxy += c * (2.0 * wu * gx * gy);
+        dens += c * wu * g2;
+        if (gq) {
+          const double *G = gq + (size_t)k * (size_t)estride() * 6 + eu * 6;
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const double t0 = c * qw * q0 * G[d], t1 = c * qw * q1 * G[2 + d], t2 = c * qw * q2 * G[4 + d];
+            sU[0][d] += t0 + t2;
+            sU[1][d] += t0 + t1;
+            sU[2][d] += t1 + t2;
+          }
+        }
+      }
+    }
+    // S1 sums against grad N: lower (-1/hx, 0), (1/hx, -1/hy), (0, 1/hy);
+    // upper (0, -1/hy), (1/hx, 0), (-1/hx, 1/hy)
+    const double ax = inv_hx, ay = inv_hy;
+    c00[0] = -Mxx * ax + (-Nxy * ay) + sL[0][0] + sU[0][0];
+    c00[1] = -Mxy * ax + (-Nyy * ay) + sL[0][1] + sU[0][1];
+    c10[0] = Mxx * ax - Mxy * ay + sL[1][0];
+    c10[1] = Mxy * ax - Myy * ay + sL[1][1];
+    c11[0] = Mxy * ay + Nxx * ax + sL[2][0] + sU[1][0];
+    c11[1] = Myy * ay + Nxy * ax + sL[2][1] + sU[1][1];
+    c01[0] = -Nxx * ax + Nxy * ay + sU[2][0];
+    c01[1] = -Nxy * ax + Nyy * ay + sU[2][1];
+    // volume part: |T| n_in / (3 V) * grad N (as Shape)
+    const double vl = area * (double)nl * (1.0 / 3.0) * inv_volume;
+    const double vu = area * (double)nu * (1.0 / 3.0) * inv_volume;
+    c00[2] = -vl * inv_hx;  c00[3] = -vu * inv_hy;
+    c10[2] = vl * inv_hx;   c10[3] = -vl * inv_hy;
+    c11[2] = vu * inv_hx;   c11[3] = vl * inv_hy;
+    c01[2] = -vu * inv_hx;  c01[3] = vu * inv_hy;
+    if (count) {
+      part[0] += dens;
+      part[1] += area * (double)(nl + nu) * (1.0 / 3.0);
+    }
+  }
+};
+
 template <class PH, int ACT>
 struct Traits {
   static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA) ? 1 : (ACT == STATS) ? 3
@@ -112,6 +229,11 @@ __device__ __forceinline__ void node_diag(const PH &ph, uint32_t w00, uint32_t w
 template <>
 __device__ __forceinline__ void node_diag<Elast>(const Elast &ph, uint32_t w00, uint32_t wm0,
                                                  uint32_t w0m, uint32_t wmm, int, int, double *d) {
+  ph.diag(w00, wm0, w0m, wmm, d);
+}
+template <>
+__device__ __forceinline__ void node_diag<Lap>(const Lap &ph, uint32_t w00, uint32_t wm0,
+                                               uint32_t w0m, uint32_t wmm, int, int, double *d) {
   ph.diag(w00, wm0, w0m, wmm, d);
 }
 template <>
@@ -166,10 +288,11 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 // ----------------------------------------------------------------------------
 template <class PH, int ACT, class W>
 __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+  constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
   constexpr int NP = Traits<PH, ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
-  constexpr int NV = (ACT == SHAPE) ? NIN / 2 : (ACT == PCGA ? 2 : 1);
+  constexpr int NF = (ACT == SHAPE) ? NIN / NC : 1;  // fields read per node (SHAPE: states)
   constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
   __shared__ double scratch[NPA * kWarps];
 
@@ -187,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   const int ic = min(max(i, 0), nx);  // clamped column: always a valid address
   const int J0 = blockIdx.y * a.seg;
   const int J1 = min(J0 + a.seg, ny + 1);
-  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 2;
+  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
 
   double beta = 0.0, alpha_prev = 0.0;
   bool first = false;
@@ -198,15 +321,14 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
       // converged: apply the pending x += alpha p of its last iteration
       const double al = s.alpha;
       if (own) {
-        double2 *xv = reinterpret_cast<double2 *>(a.xs + voff);
-        const double2 *pv = reinterpret_cast<const double2 *>(a.x2 + voff);
         for (int r = J0; r < J1; ++r) {
           const int64_t node = (int64_t)r * nxp + i;
-          double2 xo = xv[node];
-          const double2 po = pv[node];
-          xo.x = fma(al, po.x, xo.x);
-          xo.y = fma(al, po.y, xo.y);
-          xv[node] = xo;
+          double xo[NC], po[NC];
+          ld_node<NC>(a.xs + voff, node, xo);
+          ld_node<NC>(a.x2 + voff, node, po);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) xo[c] = fma(al, po[c], xo[c]);
+          st_node<NC>(a.xs + voff, node, xo);
         }
       }
       double d1[1] = {0.0}, t1[1];
@@ -223,9 +345,9 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   } else if constexpr (ACT == RESID) {
     if (a.scal[rhs].done != 0.0) return;
   }
-  const double2 *xin = reinterpret_cast<const double2 *>(a.x + voff) + ic;
-  const double2 *xin2 = reinterpret_cast<const double2 *>(ACT == PCGA ? a.x2 + voff : a.x) + ic;
-  const double2 *dvin = reinterpret_cast<const double2 *>(HAS_DINV ? a.dinv : a.x) + ic;
+  const double *xin = a.x + voff + (size_t)ic * NC;
+  const double *xin2 = (ACT == PCGA ? a.x2 + voff : a.x) + (size_t)ic * NC;
+  const double *dvin = (HAS_DINV ? a.dinv : a.x) + (size_t)ic * NC;
   const W *win = words + ic;
 
   double part[NPA];
@@ -233,13 +355,13 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   for (int t = 0; t < NPA; ++t) part[t] = 0.0;
 
   struct Raw {
-    double2 v[NV];
-    double2 dv;
-    double2 xv;  // PCGA: x of an owned node (updated with the previous alpha)
+    double v[NF + (ACT == PCGA ? 1 : 0)][NC];
+    double dv[NC];
+    double xv[NC];  // PCGA: x of an owned node (updated with the previous alpha)
     uint32_t wc;
   };
   struct Row {
-    double in[NIN], rt[NIN], raw[2], dg[2];
+    double in[NIN], rt[NIN], raw[NC], dg[NC];
     uint32_t wc;
   };
 
@@ -248,15 +370,19 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
     f.wc = node_ok ? (uint32_t)__ldg(win + off) : 0u;
     if constexpr (ACT == SHAPE) {
 #pragma unroll
-      for (int k = 0; k < NV; ++k) f.v[k] = __ldg(xin + (size_t)k * nn + off);
+      for (int k = 0; k < NF; ++k) ldg_node<NC>(xin + (size_t)k * nn * NC, off, f.v[k]);
     } else {
-      f.v[0] = __ldg(xin + off);
+      ldg_node<NC>(xin, off, f.v[0]);
       if constexpr (ACT == PCGA) {
-        f.v[1] = first ? make_double2(0.0, 0.0) : __ldg(xin2 + off);
-        if (!first && own && r >= J0 && r < J1)
-          f.xv = reinterpret_cast<const double2 *>(a.xs + voff)[off + i];
+        if (first) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) f.v[1][c] = 0.0;
+        } else {
+          ldg_node<NC>(xin2, off, f.v[1]);
+        }
+        if (!first && own && r >= J0 && r < J1) ld_node<NC>(a.xs + voff, off + i, f.xv);
       }
-      if constexpr (HAS_DINV) f.dv = __ldg(dvin + off);
+      if constexpr (HAS_DINV) ldg_node<NC>(dvin, off, f.dv);
     }
   };
 
@@ -265,32 +391,38 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
     S.wc = f.wc;
     if constexpr (ACT == SHAPE) {
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        S.in[2 * k] = f.v[k].x;
-        S.in[2 * k + 1] = f.v[k].y;
-      }
+      for (int k = 0; k < NF; ++k)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) S.in[k * NC + c] = f.v[k][c];
     } else {
       const uint32_t m = PH::mask(f.wc);
-      double2 v = f.v[0];
+      double v[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v[c] = f.v[0][c];
       if constexpr (HAS_DINV) {
-        S.dg[0] = f.dv.x;
-        S.dg[1] = f.dv.y;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) S.dg[c] = f.dv[c];
       }
       if constexpr (ACT == PCGA) {
         // z = M^-1 r with M^-1 = diag(1/D) (fem.py:303-305); p = z + beta p_old
-        v = make_double2(fma(beta, f.v[1].x, v.x * f.dv.x), fma(beta, f.v[1].y, v.y * f.dv.y));
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = fma(beta, f.v[1][c], v[c] * f.dv[c]);
         if (own && r >= J0 && r < J1) {
           const int64_t node = (int64_t)r * nxp + i;
-          reinterpret_cast<double2 *>(a.y2 + voff)[node] = v;
-          if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
-            reinterpret_cast<double2 *>(a.xs + voff)[node] =
-                make_double2(fma(alpha_prev, f.v[1].x, f.xv.x), fma(alpha_prev, f.v[1].y, f.xv.y));
+          st_node<NC>(a.y2 + voff, node, v);
+          if (!first) {  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
+            double xn[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) xn[c] = fma(alpha_prev, f.v[1][c], f.xv[c]);
+            st_node<NC>(a.xs + voff, node, xn);
+          }
         }
       }
-      S.raw[0] = v.x;
-      S.raw[1] = v.y;
-      S.in[0] = (m & 1u) ? 0.0 : v.x;
-      S.in[1] = (m & 2u) ? 0.0 : v.y;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        S.raw[c] = v[c];
+        S.in[c] = ((m >> c) & 1u) ? 0.0 : v[c];
+      }
     }
 #pragma unroll
     for (int t = 0; t < NIN; ++t) S.rt[t] = __shfl_down_sync(0xffffffffu, S.in[t], 1);
@@ -298,7 +430,7 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
 
   auto emit = [&](int r, const Row &S, const double *accv) {
     const int64_t node = (int64_t)r * nxp + i;
-    if constexpr (ACT == SHAPE) {
+    if constexpr (ACT == SHAPE) {  // outputs are velocity-space (2-component) vectors
       double2 *vc = reinterpret_cast<double2 *>(a.y);
       double2 o = make_double2(accv[0], accv[1]);
       if (a.accumulate) {
@@ -311,25 +443,37 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
       vc[node] = o;
     } else {
       const uint32_t m = PH::mask(S.wc);
-      const double yx = (m & 1u) ? S.raw[0] : accv[0];
-      const double yy = (m & 2u) ? S.raw[1] : accv[1];
+      double yv[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) yv[c] = ((m >> c) & 1u) ? S.raw[c] : accv[c];
       if constexpr (ACT == APPLY) {
-        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(yx, yy);
+        st_node<NC>(a.y + voff, node, yv);
       } else if constexpr (ACT == RESID) {
-        const double2 bv = __ldg(reinterpret_cast<const double2 *>(a.b + voff) + node);
-        const double rx = bv.x - yx, ry = bv.y - yy;
-        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(rx, ry);
-        part[0] += bv.x * bv.x + bv.y * bv.y;
-        part[1] += rx * rx + ry * ry;
-        part[2] += rx * (rx * S.dg[0]) + ry * (ry * S.dg[1]);
+        double bv[NC], rv[NC];
+        ldg_node<NC>(a.b + voff, node, bv);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          rv[c] = bv[c] - yv[c];
+          part[0] += bv[c] * bv[c];
+          part[1] += rv[c] * rv[c];
+          part[2] += rv[c] * (rv[c] * S.dg[c]);
+        }
+        st_node<NC>(a.y + voff, node, rv);
       } else if constexpr (ACT == PCGA) {
-        reinterpret_cast<double2 *>(a.y + voff)[node] = make_double2(yx, yy);
-        part[0] += S.raw[0] * yx + S.raw[1] * yy;
+        st_node<NC>(a.y + voff, node, yv);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) part[0] += S.raw[c] * yv[c];
       } else if constexpr (ACT == STATS) {
-        const double2 vv = __ldg(reinterpret_cast<const double2 *>(a.x2) + node);
-        part[0] += S.raw[0] * yx + S.raw[1] * yy;
-        part[1] += vv.x * S.raw[0] + vv.y * S.raw[1];
-        part[2] = fmax(part[2], fabs(S.raw[0]) / g.hx + fabs(S.raw[1]) / g.hy);
+        double vv[NC];
+        ldg_node<NC>(a.x2, node, vv);
+        double sp = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          part[0] += S.raw[c] * yv[c];
+          part[1] += vv[c] * S.raw[c];
+          sp += fabs(S.raw[c]) / (c == 0 ? g.hx : g.hy);
+        }
+        part[2] = fmax(part[2], sp);
       }
     }
   };
@@ -341,7 +485,8 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
     prepare(r, f, Sn);
     double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
     if constexpr (ACT == SHAPE) {
-      ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, own && (r - 1) >= J0, c00, c10, c01, c11, part);
+      ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, own && (r - 1) >= J0, i, r - 1, c00, c10, c01,
+              c11, part);
     } else {
       ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, i, r - 1, c00, c10, c01, c11);
     }

@@ -18,6 +18,9 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
 int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
+int heat_shape(const lsg_op &op, int k, const double *u, const double *weights, const double *fq,
+               const double *gq, double volume, double *vc, double *vv, double *out,
+               double *partials, uint32_t *counter, cudaStream_t st);
 int velocity_stats(const lsg_op &h1, const double *theta, const double *vec, double *out,
                    double *partials, uint32_t *counter, cudaStream_t st);
 int material(const lsg_grid &g, const double *phi, const uint8_t *bcmask, void *words,

@@ -17,6 +17,7 @@ namespace d2 {
 constexpr int kEwThreads = 256;
 constexpr int kUpd = 2;
 
+template <int NC>
 __global__ void __launch_bounds__(kEwThreads, 4)
     pcg_update(int64_t nn, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
                double *partials, uint32_t *counters) {
@@ -25,34 +26,35 @@ __global__ void __launch_bounds__(kEwThreads, 4)
   lsg_pcg_scalars &s = scal[rhs];
   if (s.done != 0.0) return;
   const double alpha = s.alpha;
-  const size_t voff = (size_t)rhs * (size_t)nn * 2;
-  double2 *rv = reinterpret_cast<double2 *>(r + voff);
-  const double2 *qv = reinterpret_cast<const double2 *>(q + voff);
-  const double2 *dv = reinterpret_cast<const double2 *>(dinv);
+  const size_t voff = (size_t)rhs * (size_t)nn * NC;
+  double *rv = r + voff;
+  const double *qv = q + voff;
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   double part[2] = {0.0, 0.0};
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < nn;
        base += stride * kUpd) {
-    double2 Q[kUpd], R[kUpd], D[kUpd];
+    double Q[kUpd][NC], R[kUpd][NC], D[kUpd][NC];
 #pragma unroll
     for (int u = 0; u < kUpd; ++u) {
       const int64_t node = base + u * stride;
       if (node < nn) {
-        Q[u] = __ldg(qv + node);
-        D[u] = __ldg(dv + node);
-        R[u] = rv[node];
+        ldg_node<NC>(qv, node, Q[u]);
+        ldg_node<NC>(dinv, node, D[u]);
+        ld_node<NC>(rv, node, R[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < kUpd; ++u) {
       const int64_t node = base + u * stride;
       if (node < nn) {
-        double2 ro = R[u];
-        ro.x = fma(-alpha, Q[u].x, ro.x);
-        ro.y = fma(-alpha, Q[u].y, ro.y);
-        rv[node] = ro;
-        part[0] += ro.x * (ro.x * D[u].x) + ro.y * (ro.y * D[u].y);
-        part[1] += ro.x * ro.x + ro.y * ro.y;
+        double ro[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          ro[c] = fma(-alpha, Q[u][c], R[u][c]);
+          part[0] += ro[c] * (ro[c] * D[u][c]);
+          part[1] += ro[c] * ro[c];
+        }
+        st_node<NC>(rv, node, ro);
       }
     }
   }
@@ -344,6 +346,20 @@ static H1 make_h1(const Geo &g, const lsg_op &op) {
   return h;
 }
 
+static Lap make_lap(const Geo &g, const lsg_op &op) {
+  const double eps = op.p[0], inside = op.p[1] > 0.0 ? op.p[1] : 1.0;
+  const double area = 0.5 * g.hx * g.hy;
+  Lap l;
+  l.w0 = area * eps;
+  l.w1 = area * (inside - eps) / 3.0;
+  l.ihx2 = 1.0 / (g.hx * g.hx);
+  l.ihy2 = 1.0 / (g.hy * g.hy);
+  return l;
+}
+
+// components per node of the operator's fields
+static int nc_of(const lsg_op &op) { return op.kind == LSG_OP_LAPLACE ? 1 : 2; }
+
 template <class PH, int ACT>
 static int launch_march(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   static int ctas_per_sm = -1;
@@ -364,6 +380,7 @@ static int dispatch_op(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   if (op.kind == LSG_OP_ELASTICITY) return launch_march<Elast, ACT>(make_elast(g, op), g, a, k, st);
   if (op.kind == LSG_OP_H1) return launch_march<H1, ACT>(make_h1(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_LAPLACE) return launch_march<Lap, ACT>(make_lap(g, op), g, a, k, st);
   set_error("unknown operator kind %d", op.kind);
   return LSG_ERR_ARG;
 }
@@ -387,11 +404,12 @@ __global__ void diag_kernel(PH ph, Geo g, const uint8_t *words, double *d) {
   const uint32_t wm0 = i > 0 ? words[node - 1] : 0u;
   const uint32_t w0m = j > 0 ? words[node - nxp] : 0u;
   const uint32_t wmm = (i > 0 && j > 0) ? words[node - nxp - 1] : 0u;
-  double dg[2];
+  constexpr int NC = PH::NC;
+  double dg[NC];
   node_diag<PH>(ph, w00, wm0, w0m, wmm, i, j, dg);
   const uint32_t m = PH::mask(w00);
-  d[node * 2] = (m & 1u) ? 1.0 : dg[0];
-  d[node * 2 + 1] = (m & 2u) ? 1.0 : dg[1];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) d[node * NC + c] = ((m >> c) & 1u) ? 1.0 : dg[c];
 }
 
 __global__ void reciprocal_kernel(int64_t n, double *d) {
@@ -403,7 +421,7 @@ int inv_diag(const lsg_op &op, double *d, cudaStream_t st) {
   int rc = diag(op, d, st);
   if (rc) return rc;
   const Geo g = geo_of(op.grid);
-  const int64_t n = 2 * (int64_t)(g.nx + 1) * (g.ny + 1);
+  const int64_t n = nc_of(op) * (int64_t)(g.nx + 1) * (g.ny + 1);
   reciprocal_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d);
   return check_launch("inv_diag2d");
 }
@@ -415,6 +433,7 @@ int diag(const lsg_op &op, double *d, cudaStream_t st) {
   const uint8_t *w = static_cast<const uint8_t *>(op.words);
   if (op.kind == LSG_OP_ELASTICITY) diag_kernel<Elast><<<nb, kEwThreads, 0, st>>>(make_elast(g, op), g, w, d);
   else if (op.kind == LSG_OP_H1) diag_kernel<H1><<<nb, kEwThreads, 0, st>>>(make_h1(g, op), g, w, d);
+  else if (op.kind == LSG_OP_LAPLACE) diag_kernel<Lap><<<nb, kEwThreads, 0, st>>>(make_lap(g, op), g, w, d);
   else { set_error("unknown operator kind %d", op.kind); return LSG_ERR_ARG; }
   return check_launch("diag2d");
 }
@@ -422,7 +441,7 @@ int diag(const lsg_op &op, double *d, cudaStream_t st) {
 int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double maxiter,
               cudaStream_t st) {
   const Geo g = geo_of(op.grid);
-  const int64_t n = 2 * (int64_t)(g.nx + 1) * (g.ny + 1);
+  const int64_t n = nc_of(op) * (int64_t)(g.nx + 1) * (g.ny + 1);
   ws.parity = 0;
   init_scalars<<<(unsigned)ceil_div(ws.k, 64), 64, 0, st>>>(ws.k, ws.scal, rtol, atol, maxiter);
   int rc = check_launch("init_scalars");
@@ -462,8 +481,12 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     a.y2 = p_new;
     int rc = dispatch_op<PCGA>(op, a, ws.k, st);
     if (rc) return rc;
-    pcg_update<<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
-                                          ws.counters);
+    if (nc_of(op) == 1)
+      pcg_update<1><<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
+                                               ws.counters);
+    else
+      pcg_update<2><<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
+                                               ws.counters);
     rc = check_launch("pcg_update2d");
     if (rc) return rc;
     ws.parity ^= 1;
@@ -526,6 +549,59 @@ int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *v
     if (left >= 4) { kb = 4; rc = shape_chunk<4>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
     else if (left >= 2) { kb = 2; rc = shape_chunk<2>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
     else { kb = 1; rc = shape_chunk<1>(g, op, uc, volume, vc, vv, out, partials, counter, chunk, st); }
+    if (rc) return rc;
+    done += kb;
+    ++chunk;
+  }
+  return LSG_OK;
+}
+
+template <int KB>
+static int heat_chunk(const Geo &g, const lsg_op &op, const double *u, const double *cw,
+                      const double *fq, const double *gq, double volume, double *vc, double *vv,
+                      double *out, double *partials, uint32_t *counter, int chunk, cudaStream_t st) {
+  HeatShape<KB> ph;
+  const double area = 0.5 * g.hx * g.hy;
+  const double eps = op.p[0], inside = op.p[1] > 0.0 ? op.p[1] : 1.0;
+  ph.nx = g.nx;
+  ph.area = area;
+  ph.inv_hx = 1.0 / g.hx;
+  ph.inv_hy = 1.0 / g.hy;
+  ph.inv_volume = 1.0 / volume;
+  ph.w0 = area * eps;
+  ph.w1 = area * (inside - eps) / 3.0;
+  for (int t = 0; t < KB; ++t) ph.cw[t] = cw[t];
+  ph.fq = fq;
+  ph.gq = gq;
+  ph.ecount = 2 * (int64_t)g.nx * g.ny;
+  MArgs a = {};
+  a.words = op.words;
+  a.x = u;
+  a.y = vc;
+  a.y2 = vv;
+  a.out = out;
+  a.partials = partials;
+  a.counters = counter;
+  a.accumulate = chunk > 0;
+  return launch_march<HeatShape<KB>, SHAPE>(ph, g, a, 1, st);
+}
+
+int heat_shape(const lsg_op &op, int k, const double *u, const double *weights, const double *fq,
+               const double *gq, double volume, double *vc, double *vv, double *out,
+               double *partials, uint32_t *counter, cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
+  const int64_t ne = 2 * (int64_t)g.nx * g.ny;
+  int done = 0, chunk = 0;
+  while (done < k) {
+    const int kb = (k - done) >= 2 ? 2 : 1;
+    const double *uc = u + (size_t)done * nn;
+    const double *fc = fq + (size_t)done * ne * 3;
+    const double *gc = gq ? gq + (size_t)done * ne * 6 : nullptr;
+    const int rc = kb == 2 ? heat_chunk<2>(g, op, uc, weights + done, fc, gc, volume, vc, vv, out,
+                                           partials, counter, chunk, st)
+                           : heat_chunk<1>(g, op, uc, weights + done, fc, gc, volume, vc, vv, out,
+                                           partials, counter, chunk, st);
     if (rc) return rc;
     done += kb;
     ++chunk;

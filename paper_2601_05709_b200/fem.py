@@ -21,7 +21,7 @@ import torch
 from . import _lib
 from .errors import ConfigError, SolverError
 
-__all__ = ["FunctionSpace", "FemField", "DirichletSet", "ElasticityOperator", "H1Operator",
+__all__ = ["FunctionSpace", "FemField", "DirichletSet", "ElasticityOperator", "H1Operator", "LaplaceOperator",
            "LinearProblem", "solve_linear", "solve_batched", "CG_RTOL", "CG_ATOL",
            "CG_ITER_FACTOR", "to_device"]
 
@@ -143,10 +143,11 @@ class _Operator:
     """Matrix-free operator on a vector space: the ``matrix`` slot of a problem."""
 
     kind = None
+    scalar = False  # True for operators on scalar (temperature) spaces
 
     def __init__(self, space):
-        if space.value_rank != space.dim:
-            raise ConfigError("operators act on vector spaces")
+        if space.value_rank != (1 if self.scalar else space.dim):
+            raise ConfigError("this operator acts on " + ("scalar" if self.scalar else "vector") + " spaces")
         self.space = space
         self.grid = space.mesh.grid
 
@@ -206,6 +207,32 @@ class ElasticityOperator(_Operator):
                   _lib.ptr(self.words), _lib.stream())
         self._cop = _lib.make_op(self.kind, self.grid, self.words,
                                  (self.lame[0], self.lame[1], self.ersatz, self.inside))
+
+    def _op(self):
+        return self._cop
+
+
+class LaplaceOperator(_Operator):
+    """Two-phase diffusion (A grad u, grad v) of the heat models, Dirichlet-eliminated
+    (``models/heat.py:113-119``, ``fem.py:388-394``); A = inside where phi < 0 at a
+    quadrature point, ``contrast`` elsewhere, averaged per triangle.  2D only, as
+    the reference."""
+
+    kind = _lib.LSG_OP_LAPLACE
+    scalar = True
+
+    def __init__(self, space, phi_values, contrast, bc=None, inside=1.0):
+        super().__init__(space)
+        if space.dim != 2:
+            raise ConfigError("the heat models are 2D (models/heat.py), as the reference")
+        self.contrast = float(contrast)
+        self.inside = float(inside)
+        self.bc = bc
+        self.bcmask = bc.node_mask(space) if bc is not None and len(bc) else None
+        self.words = torch.empty(space.mesh.num_vertices, dtype=torch.uint8, device="cuda")
+        _lib.call("lsg_material", self.grid, _lib.ptr(to_device(phi_values)), _lib.ptr(self.bcmask),
+                  _lib.ptr(self.words), _lib.stream())
+        self._cop = _lib.make_op(self.kind, self.grid, self.words, (self.contrast, self.inside))
 
     def _op(self):
         return self._cop

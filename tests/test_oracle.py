@@ -303,3 +303,41 @@ class TestOracle3D:
         s1 = fem.Space(g, 1)
         M = s1.assemble_matrix(fem.mass_elements(s1))
         assert M.sum() == pytest.approx(2.0, rel=1e-13)
+
+
+# -- heat models (reference models/heat.py), pinned to tests/golden/reference_heat.npz --------
+def _heat_oracle():
+    from oracle import model as om
+    from oracle.grid import Grid
+    from heat_cases import BOUNDS, NX, NY, RULES, grad_a, phi_fn, src_a, src_b
+    grid = Grid(BOUNDS[:2], BOUNDS[2:], (NX, NY), RULES)
+    space = om.fem.Space(grid, 1)
+    pts = space.quad_points.reshape(-1, 2)
+    fa = src_a(pts).reshape(-1, 3)
+    ga = grad_a(pts).reshape(-1, 3, 2)
+    fb = src_b(pts).reshape(-1, 3)
+    ground_a = np.unique(grid.boundary_facets[grid.facets_with_tag(1)])
+    ground_b = np.unique(grid.boundary_facets[grid.facets_with_tag((2, 3))])
+    model = om.Heat(grid, [(0.7, ground_a, fa, ga), (None, ground_b, fb, None)], 0.6)
+    return grid, model, phi_fn(grid.vertices)
+
+
+def test_heat_oracle_matches_reference():
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_heat.npz"))
+    from oracle import model as om
+    grid, model, phi = _heat_oracle()
+    np.testing.assert_allclose(phi, g["phi"], rtol=0, atol=0)
+    np.testing.assert_allclose(np.stack([t[4] for t in model.terms]), g["loads"], rtol=1e-13, atol=1e-16)
+    states, _ = model.solve_states(phi)
+    for u, ref in zip(states, g["states"]):
+        assert np.linalg.norm(u - ref) <= 1e-8 * np.linalg.norm(ref)
+    states = list(g["states"])  # evaluate the functionals on the reference states
+    assert model.cost(phi, states) == pytest.approx(float(g["J"][0]), rel=1e-12)
+    assert model.constraint(phi) == pytest.approx(float(g["C"][0]), rel=1e-14)
+    s0, s1 = model.tensors(phi, states)
+    np.testing.assert_allclose(s0, g["S0"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(s1, g["S1"], rtol=1e-12, atol=1e-12)
+    vspace = om.fem.Space(grid, 2)
+    vec = om.derivative_vector(vspace, s1=s1, s0=s0)
+    assert np.linalg.norm(vec - g["vec_cost"]) <= 1e-12 * np.linalg.norm(g["vec_cost"])
