@@ -219,6 +219,40 @@ int lsg_heat_shape(const lsg_op *op, int32_t k, const double *u, const double *w
                    double *vec_vol, double *out, double *partials, uint32_t *counter,
                    void *stream);
 
+/* Inverse-elasticity model (models/inverse.py, 2D), k measurement pairs,
+ * fields (k, 2N) interleaved.
+ *
+ * lsg_inverse_misfit replaces InverseElasticityModel._misfits / adjoint /
+ * cost (inverse.py:180-233): with e = u - v - g and f = u - g it writes the
+ * adjoint right-hand sides head = -alpha M e - beta M_G f (zeroed on the dofs
+ * flagged in partial_mask, bit c = component c) and tail = alpha M e (zeroed
+ * on the whole boundary), and out[0] = J = sum_k alpha/2 e.Me + beta/2 f.M_G f.
+ * M = P1 mass (edge-midpoint rule), M_G = facet mass of the measured facets:
+ * facet_flags[node] bit 0 = facet (node, node+1) measured, bit 1 = facet
+ * (node, node+nx+1).  partials/counter: >= 1024 doubles / one uint32 (zero).
+ *
+ * lsg_inverse_tensors replaces InverseElasticityModel.derivative
+ * (inverse.py:235-279): S0 (E,3,2) and S1 (E,3,2,2) at the quadrature points,
+ * summed over the pairs; p, q = the two adjoint families; proj (k,3,2N) =
+ * nodal projections of eps_xx, eps_xy, eps_yy of g stored as (value, 0);
+ * A_q = a_in where phi < 0 at the point, a_out elsewhere.
+ *
+ * lsg_strain_projection_rhs writes the right-hand sides of those projections
+ * (inverse.py:142-155): out (k,3,2N), sum over the triangles at a node of
+ * |T|/3 eps_cc(g), as (value, 0). */
+int lsg_inverse_misfit(const lsg_grid *g, int32_t k, const double *u, const double *v,
+                       const double *measured, const uint8_t *facet_flags,
+                       const uint8_t *partial_mask, double alpha, double beta, double *head,
+                       double *tail, double *out, double *partials, uint32_t *counter,
+                       void *stream);
+int lsg_inverse_tensors(const lsg_grid *g, int32_t k, const double *u, const double *v,
+                        const double *p, const double *q, const double *measured,
+                        const double *proj, const double *phi, double a_in, double a_out,
+                        double lam, double mu, double alpha, double *s0, double *s1,
+                        void *stream);
+int lsg_strain_projection_rhs(const lsg_grid *g, int32_t k, const double *measured, double *out,
+                              void *stream);
+
 /* S1 of the cost per element and quadrature point, (E, nq, dim, dim), for
  * parity with ComplianceModel.derivative's tensor (compliance.py:128-139):
  * S1_q = A_q sum_k (2 G_k^T sigma_k - (sigma_k:eps_k) I), A_q from phi. */

@@ -20,7 +20,13 @@ Restates, dimension-generically:
   term (``:59-76,116-122``), adjoint -c_t u_t (``:124-128``),
   J = sum_t c_t int A |grad u_t|^2 (``:130-138``), S0 = sum_t c_t 2 u grad f,
   S1 = sum_t c_t ((2 u f - A |grad u|^2) I + 2 A grad u (x) grad u)
-  (``:143-166``).
+  (``:143-166``);
+* ``InverseElasticityModel`` (``models/inverse.py:78-279``): A_q = kappa chi
+  + (1 - chi) (``:102``), forced states (partial clamp) and lifted
+  corrections v in H^1_0 with rhs -K g (``:160-178``), misfit, adjoint
+  right-hand sides and J (``:180-233``), strain projections (``:142-155``),
+  S0/S1 (``:235-279``); ``dirichlet_extension`` and
+  ``generate_measurements`` (``:282-353``).
 """
 
 from dataclasses import dataclass, replace
@@ -178,6 +184,139 @@ class Heat:
             outer = np.einsum("ti,tj->tij", g, g)
             s1 += w * (scal[:, :, None, None] * np.eye(2) + 2.0 * a_q[:, :, None, None] * outer[:, None, :, :])
         return s0, s1
+
+
+EDGE_GAUSS = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
+EDGE_BASIS = np.stack([1.0 - EDGE_GAUSS, EDGE_GAUSS], axis=1)
+
+
+def _facet_mass_vector(grid, facet_ids, values):
+    """sum_f int_f (vector field) N_a with the 2-point Gauss rule (``fem.py:441-448``)."""
+    facets = grid.boundary_facets[facet_ids]
+    lengths = grid.facet_measures()[facet_ids]
+    nodal = np.asarray(values).reshape(-1, 2)[facets]  # (nf, 2 nodes, 2 comps)
+    tr = np.einsum("qi,fic->fqc", EDGE_BASIS, nodal)
+    elems = np.einsum("fq,fqc,qa->fac", np.repeat((lengths / 2.0)[:, None], 2, axis=1), tr, EDGE_BASIS)
+    out = np.zeros(2 * grid.num_vertices)
+    dofs = 2 * facets[:, :, None] + np.arange(2)[None, None, :]
+    np.add.at(out, dofs.reshape(len(facets), -1), elems.reshape(len(facets), -1))
+    return out, tr, lengths
+
+
+class Inverse:
+    """Kohn-Vogelius inclusion recovery (reference ``models/inverse.py``), 2D."""
+
+    def __init__(self, grid, partial_dofs, measured_facets, loads, measured, contrast=10.0,
+                 alpha=1.0, beta=1.0, lame=(1.25, 1.0)):
+        self.grid = grid
+        self.space = fem.Space(grid, 2)
+        self.scalar = fem.Space(grid, 1)
+        self.partial = np.asarray(partial_dofs, dtype=np.int64)
+        self.total = fem.clamp_dofs(self.space, np.arange(len(grid.boundary_facets)))
+        self.mfacets = np.asarray(measured_facets, dtype=np.int64)
+        self.loads = [np.asarray(b, dtype=float) for b in loads]
+        self.g = [np.asarray(v, dtype=float) for v in measured]
+        self.contrast, self.alpha, self.beta = float(contrast), float(alpha), float(beta)
+        self.lame = tuple(float(v) for v in lame)
+        mass = self.scalar.assemble_matrix(fem.mass_elements(self.scalar))
+        self.proj = [self._project(mass, g) for g in self.g]
+
+    def _project(self, mass, g):
+        """Gradients of the nodal projections of eps(g): (E, 2, 2, 2) (``inverse.py:142-155``)."""
+        eps = fem.strain(self.space.grad_at_quad(g))
+        nt, nq = self.scalar.quad_weights.shape
+        out = np.empty((nt, 2, 2, 2))
+        for i, j in ((0, 0), (0, 1), (1, 1)):
+            comp_q = np.broadcast_to(eps[:, i, j][:, None], (nt, nq))
+            rhs = self.scalar.assemble_vector(np.einsum("tq,qa->ta", self.scalar.quad_weights * comp_q,
+                                                        self.scalar.bary))
+            nodal, _ = fem.jacobi_pcg(mass, rhs)
+            out[:, i, j, :] = self.scalar.grad_at_quad(nodal)
+        out[:, 1, 0, :] = out[:, 0, 1, :]
+        return out
+
+    def a_q(self, phi):
+        chi = fem.phi_at_quad_sign(self.space, phi).astype(float)
+        return self.contrast * chi + (1.0 - chi)
+
+    def matrix(self, phi):
+        return self.space.assemble_matrix(fem.elasticity_elements(self.space, self.a_q(phi), self.lame))
+
+    def state_systems(self, phi):
+        K = self.matrix(phi)
+        forced = [fem.dirichlet_eliminate(K, b, self.partial) for b in self.loads]
+        lifted = [fem.dirichlet_eliminate(K, -(K @ g), self.total) for g in self.g]
+        return forced + lifted
+
+    def solve(self, systems):
+        return [fem.jacobi_pcg(A, b)[0] for A, b in systems]
+
+    def misfit(self, states):
+        n = len(self.g)
+        out = []
+        for g, u, v in zip(self.g, states[:n], states[n:]):
+            e = u - v - g
+            me = self.space.assemble_vector(np.einsum(
+                "tq,tqc,qa->tac", self.space.quad_weights,
+                np.einsum("qi,tic->tqc", self.space.bary, e.reshape(-1, 2)[self.grid.elements]),
+                self.space.bary).reshape(len(self.grid.elements), -1))
+            mf, tr, lengths = _facet_mass_vector(self.grid, self.mfacets, u - g)
+            out.append((e, me, u - g, mf))
+        return out
+
+    def cost(self, states):
+        total = 0.0
+        for e, me, f, mf in self.misfit(states):
+            total += 0.5 * self.alpha * float(e @ me) + 0.5 * self.beta * float(f @ mf)
+        return total
+
+    def adjoint_systems(self, phi, states):
+        K = self.matrix(phi)
+        mis = self.misfit(states)
+        head = [fem.dirichlet_eliminate(K, -self.alpha * me - self.beta * mf, self.partial)
+                for _, me, _, mf in mis]
+        tail = [fem.dirichlet_eliminate(K, self.alpha * me, self.total) for _, me, _, _ in mis]
+        return head + tail
+
+    def tensors(self, phi, states, adjoints):
+        a_q = self.a_q(phi)
+        n = len(self.g)
+        nt, nq = a_q.shape
+        s0 = np.zeros((nt, nq, 2))
+        s1 = np.zeros((nt, nq, 2, 2))
+        sp_ = self.space
+        for k in range(n):
+            u, v, g = states[k], states[n + k], self.g[k]
+            p, q = adjoints[k], adjoints[n + k]
+            bulk = np.einsum("qi,tic->tqc", sp_.bary, (u - v - g).reshape(-1, 2)[self.grid.elements])
+            ju, jv, jp, jq, jg = (sp_.grad_at_quad(x) for x in (u, v, p, q, g))
+            su, spp, sq = (fem.stress(fem.strain(j), self.lame) for j in (ju, jp, jq))
+            sy = fem.stress(fem.strain(jv + jg), self.lame)
+            s0 -= self.alpha * np.einsum("tji,tqj->tqi", jg, bulk)
+            drift = np.einsum("tij,tijk->tk", sq, self.proj[k])
+            s0 += a_q[:, :, None] * drift[:, None, :]
+            scal = 0.5 * self.alpha * np.einsum("tqc,tqc->tq", bulk, bulk)
+            pairing = (np.einsum("tij,tij->t", su, fem.strain(jp))
+                       + np.einsum("tij,tij->t", sy, fem.strain(jq)))
+            scal = scal + a_q * pairing[:, None]
+            mat = (np.einsum("tki,tkj->tij", ju, spp) + np.einsum("tki,tkj->tij", jp, su)
+                   + np.einsum("tki,tkj->tij", jv, sq) + np.einsum("tki,tkj->tij", jq, sy))
+            s1 += scal[:, :, None, None] * np.eye(2)
+            s1 -= a_q[:, :, None, None] * mat[:, None, :, :]
+        return s0, s1
+
+
+def dirichlet_extension(grid, facet_ids, traces):
+    """Harmonic extension (``inverse.py:282-313``): vector Laplace, values on the facet nodes."""
+    space = fem.Space(grid, 2)
+    nodes = np.unique(grid.boundary_facets[facet_ids])
+    dofs = np.column_stack([2 * nodes, 2 * nodes + 1]).reshape(-1)
+    K = space.assemble_matrix(fem.stiffness_elements(space))
+    out = []
+    for tr in traces:
+        A, b = fem.dirichlet_eliminate(K, np.zeros(space.dof_count), dofs, np.asarray(tr)[dofs])
+        out.append(fem.jacobi_pcg(A, b)[0])
+    return out
 
 
 def derivative_vector(space, s1=None, s0=None):

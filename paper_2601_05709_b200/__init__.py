@@ -18,7 +18,9 @@ from .fem import (DirichletSet, ElasticityOperator, FemField, FunctionSpace, H1O
 from .levelset import InitialLevelSpec, LevelSetField, initial_level, reinitialize, transport
 from .mesh import (BoxMesh, RectMesh, build_box_mesh, build_rect_mesh, mesh_diameter,
                    tag_boundary)
-from .models import ComplianceModel, CompliancePlusModel, HeatModel, HeatPlusModel, HeatTerm
+from .models import (ComplianceModel, CompliancePlusModel, HeatModel, HeatPlusModel, HeatTerm,
+                     InverseElasticityModel, MeasurementPair, dirichlet_extension,
+                     generate_measurements)
 from .ppl import combine_derivatives, lagrangian_value, ppl_init, ppl_update
 from .velocity import BilinearSpec, DerivativePair, VelocityResult, VelocitySolver
 
@@ -28,7 +30,8 @@ __all__ = [
     "build_box_mesh", "mesh_diameter", "tag_boundary", "InitialLevelSpec", "LevelSetField",
     "initial_level", "reinitialize", "transport", "FunctionSpace", "FemField", "DirichletSet",
     "ElasticityOperator", "H1Operator", "LaplaceOperator", "LinearProblem", "solve_linear", "solve_batched",
-    "ComplianceModel", "CompliancePlusModel", "HeatModel", "HeatPlusModel", "HeatTerm", "BilinearSpec", "DerivativePair", "VelocityResult",
+    "ComplianceModel", "CompliancePlusModel", "HeatModel", "HeatPlusModel", "HeatTerm", "InverseElasticityModel",
+    "MeasurementPair", "dirichlet_extension", "generate_measurements", "BilinearSpec", "DerivativePair", "VelocityResult",
     "VelocitySolver", "combine_derivatives", "lagrangian_value", "ppl_init", "ppl_update",
 ]
 

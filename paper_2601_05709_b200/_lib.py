@@ -81,6 +81,10 @@ SIGNATURES = {
     "lsg_pcg_finish": (ctypes.c_int, [_O, _W, _P]),
     "lsg_shape_rhs": (ctypes.c_int, [_O, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P]),
     "lsg_heat_shape": (ctypes.c_int, [_O, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
+    "lsg_inverse_misfit": (ctypes.c_int, [_G, _I, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P, _P]),
+    "lsg_inverse_tensors": (ctypes.c_int, [_G, _I, _P, _P, _P, _P, _P, _P, _P, _D, _D, _D, _D, _D,
+                                           _P, _P, _P]),
+    "lsg_strain_projection_rhs": (ctypes.c_int, [_G, _I, _P, _P, _P]),
     "lsg_s1_tensor": (ctypes.c_int, [_O, _I, _P, _P, _P, _P]),
     "lsg_tensor_rhs": (ctypes.c_int, [_G, _P, _P, _P, _P]),
     "lsg_velocity_rhs": (ctypes.c_int, [_O, _P, _P, _D, _P, _P]),

@@ -250,6 +250,51 @@ int lsg_heat_shape(const lsg_op *op, int32_t k, const double *u, const double *w
                         counter, S(stream));
 }
 
+static int need_2d(const lsg_grid *g, const char *what) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (g->dim != 2) { set_error("%s is 2D only (models/inverse.py), as the reference", what); return LSG_ERR_ARG; }
+  return LSG_OK;
+}
+
+int lsg_inverse_misfit(const lsg_grid *g, int32_t k, const double *u, const double *v,
+                       const double *measured, const uint8_t *facet_flags,
+                       const uint8_t *partial_mask, double alpha, double beta, double *head,
+                       double *tail, double *out, double *partials, uint32_t *counter,
+                       void *stream) {
+  int rc = need_2d(g, "inverse_misfit");
+  if (rc) return rc;
+  if (k < 1 || !u || !v || !measured || !facet_flags || !head || !tail || !out) {
+    set_error("inverse_misfit: missing arrays or k < 1");
+    return LSG_ERR_ARG;
+  }
+  return inverse_misfit(*g, k, u, v, measured, facet_flags, partial_mask, alpha, beta, head, tail,
+                        out, partials, counter, S(stream));
+}
+
+int lsg_inverse_tensors(const lsg_grid *g, int32_t k, const double *u, const double *v,
+                        const double *p, const double *q, const double *measured,
+                        const double *proj, const double *phi, double a_in, double a_out,
+                        double lam, double mu, double alpha, double *s0, double *s1,
+                        void *stream) {
+  int rc = need_2d(g, "inverse_tensors");
+  if (rc) return rc;
+  if (k < 1 || !u || !v || !p || !q || !measured || !proj || !phi || !s0 || !s1) {
+    set_error("inverse_tensors: missing arrays or k < 1");
+    return LSG_ERR_ARG;
+  }
+  return inverse_tensors(*g, k, u, v, p, q, measured, proj, phi, a_in, a_out, lam, mu, alpha, s0,
+                         s1, S(stream));
+}
+
+int lsg_strain_projection_rhs(const lsg_grid *g, int32_t k, const double *measured, double *out,
+                              void *stream) {
+  int rc = need_2d(g, "strain_projection_rhs");
+  if (rc) return rc;
+  if (k < 1 || !measured || !out) { set_error("strain_projection_rhs: missing arrays"); return LSG_ERR_ARG; }
+  return strain_projection_rhs(*g, k, measured, out, S(stream));
+}
+
 int lsg_s1_tensor(const lsg_op *op, int32_t k, const double *u, const double *phi, double *s1,
                   void *stream) {
   int rc = check_op(op);

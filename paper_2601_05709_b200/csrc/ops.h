@@ -78,6 +78,17 @@ int reinit_rhs(const lsg_op &op, double *rhs, cudaStream_t st);
 int bicgstab(const lsg_op &op, const double *b, double *x, double *work, double rtol, int maxit,
              int *iters, double *resid, cudaStream_t st);
 }  // namespace pg
+// inverse-elasticity model (inverse2d.cu), 2D
+int inverse_misfit(const lsg_grid &grid, int k, const double *u, const double *v, const double *g,
+                   const uint8_t *flags, const uint8_t *pmask, double alpha, double beta,
+                   double *head, double *tail, double *out, double *partials, uint32_t *counter,
+                   cudaStream_t st);
+int inverse_tensors(const lsg_grid &grid, int k, const double *u, const double *v, const double *p,
+                    const double *q, const double *g, const double *proj, const double *phi,
+                    double a_in, double a_out, double lam, double mu, double alpha, double *s0,
+                    double *s1, cudaStream_t st);
+int strain_projection_rhs(const lsg_grid &grid, int k, const double *g, double *out,
+                          cudaStream_t st);
 int reinit(const lsg_grid &g, const double *phi_in, double dt, int nsub, double h, double *phi_out,
            double *tmp, double *sgn, cudaStream_t st);
 

@@ -41,16 +41,25 @@ def traction_vector(space, facet_ids, g):
     """
     mesh = space.mesh
     d = mesh.dim
-    g = np.asarray(g, dtype=float)
-    if g.shape != (d,):
-        raise ConfigError(f"traction must be a {d}-vector, got shape {g.shape}")
     facets = mesh.boundary_facets[facet_ids]
     meas = mesh.facet_measures[facet_ids]
+    if callable(g):  # sampled at the facet Gauss points (boundary_vector_load, fem.py:441-448)
+        if d != 2:
+            raise ConfigError("callable tractions are 2D only, as the reference")
+        gp = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
+        a, b = mesh.vertices[facets[:, 0]], mesh.vertices[facets[:, 1]]
+        pts = a[:, None, :] + gp[None, :, None] * (b - a)[:, None, :]
+        g_q = np.asarray(g(pts), dtype=float).reshape(len(facets), 2, 2)
+    else:
+        g = np.asarray(g, dtype=float)
+        if g.shape != (d,):
+            raise ConfigError(f"traction must be a {d}-vector, got shape {g.shape}")
+        g_q = np.broadcast_to(g, (len(facets), 2, d))
     if d == 2:
         gp = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
         basis = np.stack([1.0 - gp, gp], axis=1)
         w = np.repeat((meas / 2.0)[:, None], 2, axis=1)
-        elems = np.einsum("fqc,qa->fac", w[:, :, None] * np.broadcast_to(g, (len(facets), 2, 2)), basis)
+        elems = np.einsum("fqc,qa->fac", w[:, :, None] * g_q, basis)
     else:
         elems = np.broadcast_to((meas / 3.0)[:, None, None] * g[None, None, :], (len(facets), 3, 3))
     out = np.zeros(space.dof_count)

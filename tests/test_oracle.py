@@ -341,3 +341,61 @@ def test_heat_oracle_matches_reference():
     vspace = om.fem.Space(grid, 2)
     vec = om.derivative_vector(vspace, s1=s1, s0=s0)
     assert np.linalg.norm(vec - g["vec_cost"]) <= 1e-12 * np.linalg.norm(g["vec_cost"])
+
+
+# -- inverse-elasticity model (reference models/inverse.py), pinned to reference_inverse.npz --
+def test_inverse_oracle_matches_reference():
+    import os
+    from inverse_cases import (BOUNDS, COARSE, CONTRAST, FINE, FIXED, FORCES, LAME, MEASURED,
+                               guess, inclusion, rules)
+    from oracle import model as om
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_inverse.npz"))
+    coarse = Grid(BOUNDS[:2], BOUNDS[2:], COARSE, rules())
+    fine = Grid(BOUNDS[:2], BOUNDS[2:], FINE, rules())
+    # twin measurements: fine solve with the true inclusion, injection, harmonic extension
+    fspace = fem.Space(fine, 2)
+    fmodel = om.Inverse(fine, fem.clamp_dofs(fspace, fine.facets_with_tag(FIXED)),
+                        fine.facets_with_tag(MEASURED),
+                        [fem.boundary_traction_vector(fspace, fine.facets_with_tag(t), tr) for tr, t in FORCES],
+                        [np.zeros(fspace.dof_count)], contrast=CONTRAST, lame=LAME)
+    K = fmodel.matrix(inclusion(fine.vertices))
+    inj = np.array([np.flatnonzero((np.abs(fine.vertices - v) < 1e-12).all(axis=1))[0]
+                    for v in coarse.vertices])
+    traces = []
+    for b in fmodel.loads:
+        A, rhs = fem.dirichlet_eliminate(K, b, fmodel.partial)
+        traces.append(fem.jacobi_pcg(A, rhs)[0].reshape(-1, 2)[inj].reshape(-1))
+    ext = om.dirichlet_extension(coarse, coarse.facets_with_tag((FIXED,) + MEASURED), traces)
+    for x, ref in zip(ext, g["measured"]):
+        assert rel_l2(x, ref) <= 1e-8
+    e2 = om.dirichlet_extension(coarse, coarse.facets_with_tag((1, 3)), [g["ext_trace"]])[0]
+    assert rel_l2(e2, g["ext_out"]) <= 1e-9
+    # the model pieces on the reference's own inputs
+    cspace = fem.Space(coarse, 2)
+    model = om.Inverse(coarse, fem.clamp_dofs(cspace, coarse.facets_with_tag(FIXED)),
+                       coarse.facets_with_tag(MEASURED),
+                       [fem.boundary_traction_vector(cspace, coarse.facets_with_tag(t), tr) for tr, t in FORCES],
+                       list(g["measured"]), contrast=CONTRAST, lame=LAME)
+    phi = g["phi"]
+    np.testing.assert_array_equal(phi, guess(coarse.vertices))
+    systems = model.state_systems(phi)
+    # the reference's LinearProblem.rhs is the raw right-hand side (before elimination)
+    raw = model.loads + [-(model.matrix(phi) @ x) for x in model.g]
+    np.testing.assert_allclose(np.stack(raw), g["state_rhs"], rtol=1e-12, atol=1e-14)
+    states = model.solve(systems)
+    for x, ref in zip(states, g["states"]):
+        assert rel_l2(x, ref) <= 1e-8
+    states = list(g["states"])
+    assert model.cost(states) == pytest.approx(float(g["J"][0]), rel=1e-12)
+    mis = model.misfit(states)
+    head = [-model.alpha * me - model.beta * mf for _, me, _, mf in mis]
+    tail = [model.alpha * me for _, me, _, _ in mis]
+    np.testing.assert_allclose(np.stack(head + tail), g["adjoint_rhs"], rtol=1e-12, atol=1e-15)
+    adjoints = model.solve(model.adjoint_systems(phi, states))
+    for x, ref in zip(adjoints, g["adjoints"]):
+        assert rel_l2(x, ref) <= 1e-7
+    s0, s1 = model.tensors(phi, states, list(g["adjoints"]))
+    np.testing.assert_allclose(s0, g["S0"], rtol=1e-9, atol=1e-12 * np.abs(g["S0"]).max())
+    np.testing.assert_allclose(s1, g["S1"], rtol=1e-9, atol=1e-12 * np.abs(g["S1"]).max())
+    vec = derivative_vector(cspace, s1=s1, s0=s0)
+    assert rel_l2(vec, g["vec"]) <= 1e-9
