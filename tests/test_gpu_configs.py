@@ -137,3 +137,53 @@ def test_cfg4_full_size_properties():
     res = VelocitySolver(model.bilinear_form(), model.space).solve(pair)
     assert res.form_value > 0
     assert abs(res.derivative + res.form_value) <= 1e-8 * (1 + res.form_value)
+
+
+# -- the same configurations from the shipped TOML files (paper_2601_05709_b200.config) ------
+@pytest.mark.parametrize("name,n", [("cfg1", (40, 20)), ("cfg5", (24, 12, 12))])
+def test_toml_config_builds_the_coded_case(name, n):
+    import os
+    from dataclasses import replace
+    from paper_2601_05709_b200.config import build_initial, build_mesh, build_model, parse_config
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = parse_config(os.path.join(root, "configs", f"{name}.toml"))
+    mesh_kw = dict(nx=n[0], ny=n[1]) if len(n) == 2 else dict(nx=n[0], ny=n[1], nz=n[2])
+    cfg = replace(cfg, mesh=replace(cfg.mesh, **mesh_kw))
+    mesh = build_mesh(cfg)
+    model, phi = build_model(cfg, mesh), build_initial(cfg, mesh)
+    c = configs.case(name, scale=4 if name == "cfg1" else 8)
+    _, model2, phi2, _ = configs.build(c)
+    np.testing.assert_array_equal(host(phi.values), host(phi2.values))
+    np.testing.assert_allclose(host(model.load_vectors), host(model2.load_vectors), rtol=1e-14, atol=0)
+    s1, s2 = lsg.solve_concurrent(model.pde(phi)), lsg.solve_concurrent(model2.pde(phi2))
+    assert model.cost(phi, s1) == pytest.approx(model2.cost(phi2, s2), rel=1e-12)
+
+
+def test_toml_inverse_and_heat_models_run():
+    from paper_2601_05709_b200.config import build_initial, build_mesh, build_model, config_from_dict
+    inverse = {
+        "model": {"kind": "inverse", "fixed_tag": 1, "measured_tag": [2, 3, 4, 5], "contrast": 10.0,
+                  "twin": {"center": [1.0, 0.5], "radius": 0.25, "refine": 2},
+                  "force": [{"traction": [1.0, 0.0], "tag": 3}, {"traction": [0.0, -1.0], "tag": 4}]},
+        "mesh": {"bounds": [0.0, 0.0, 2.0, 1.0], "nx": 16, "ny": 8},
+        "boundary": [{"tag": 3, "side": "left", "span": [0.25, 0.75]},
+                     {"tag": 4, "side": "top", "span": [0.75, 1.25]},
+                     {"tag": 5, "side": "right", "span": [0.25, 0.75]},
+                     {"tag": 1, "side": "bottom"}, {"tag": 2, "side": "all"}],
+        "initial": {"centers": [[0.9, 0.6]], "radii": [0.35], "factor": -1.0},
+        "run": {"niter": 3, "start_to_check": 3, "lv_time": [1e-3, 10.0], "lv_iter": [8, 32]},
+    }
+    heat = {
+        "model": {"kind": "heat", "volume": 0.5, "fixed_tag": 1,
+                  "source": {"kind": "radial", "center": [0.5, 0.5], "amplitude": 25.0, "cutoff": 0.2}},
+        "mesh": {"bounds": [0.0, 0.0, 1.0, 1.0], "nx": 16, "ny": 16},
+        "boundary": [{"tag": 1, "side": "all"}],
+        "initial": {"centers": [[0.25, 0.25], [0.75, 0.75]], "radii": [0.15, 0.15]},
+        "run": {"niter": 3, "start_to_check": 3, "smooth": True},
+    }
+    for doc in (inverse, heat):
+        cfg = config_from_dict(doc)
+        mesh = build_mesh(cfg)
+        model, phi = build_model(cfg, mesh), build_initial(cfg, mesh)
+        _, hist = lsg.run(model, phi, cfg.params, timing=False)
+        assert len(hist) == 3 and all(np.isfinite(r.cost) for r in hist)
