@@ -40,7 +40,7 @@ constexpr int kRowSlot = 98;  // doubles: 49 chunks of 16 bytes
 
 template <class PH, int ACT>
 struct Stage {
-  static constexpr int NS = (ACT == PCGA) ? 4 : (ACT == RESID) ? 2 : PH::NIN / 3;
+  static constexpr int NS = (ACT == PCGA) ? 4 : (ACT == RESID) ? 2 : PH::NIN / 3;  // PCGQ: p
   static constexpr int NOUT = PH::NOUT;
   static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NS * kRowSlot;
   static constexpr size_t words = (size_t)3 * (kWarps + 1) * 32;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     first = s.first != 0.0;
     beta = s.beta;
     alpha_prev = s.alpha;
-  } else if constexpr (ACT == RESID) {
+  } else if constexpr (ACT == RESID || ACT == PCGQ) {
     if (a.scal[rhs].done != 0.0) return;
   }
 
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
           part[1] += r * r;
           part[2] += r * (r * dg[q]);
         }
-      } else if constexpr (ACT == PCGA) {
+      } else if constexpr (ACT == PCGA || ACT == PCGQ) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           a.y[voff + node * 3 + q] = yv[q];

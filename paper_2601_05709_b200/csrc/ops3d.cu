@@ -24,6 +24,7 @@
 // H1 word (lsg_h1_words): bits 4m..4m+3 = frozen flags of tet m's quadrature
 // points, bit 24 = cell valid, bit 25 = Dirichlet (all components).
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "ops.h"
@@ -345,7 +346,8 @@ struct Shape {
   }
 };
 
-enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4 };
+// PCGQ: the apply half of a split pass A (q = A p, p.q; p formed by pcg_prep)
+enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4, PCGQ = 5 };
 
 struct MArgs {
   const uint32_t *words;
@@ -362,8 +364,8 @@ struct MArgs {
 
 template <int ACT>
 struct Traits {
-  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA) ? 1 : (ACT == STATS) ? 3
-                                                                     : (ACT == SHAPE) ? 2 : 0;
+  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA || ACT == PCGQ) ? 1
+                         : (ACT == STATS) ? 3 : (ACT == SHAPE) ? 2 : 0;
   static constexpr unsigned MAXMASK = (ACT == STATS) ? 4u : 0u;
 };
 
@@ -383,7 +385,7 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
     } else if (sqrt(tot[1]) < s.atol) {
       s.done = 1.0;
     }
-  } else if constexpr (ACT == PCGA) {
+  } else if constexpr (ACT == PCGA || ACT == PCGQ) {
     lsg_pcg_scalars &s = a.scal[rhs];
     s.pq = tot[0];
     s.alpha = s.rho / tot[0];
@@ -460,6 +462,44 @@ __global__ void __launch_bounds__(kEwThreads, 4)
         s.beta = tot[0] / s.rho;
         s.rho = tot[0];
         s.first = 0.0;
+      }
+    }
+  }
+}
+
+// Split pass A, first half (elementwise, HBM-bound): p = D^-1 r + beta p_old
+// and the pending x += alpha_prev p_old of the previous iteration.  The
+// stencil half (march3s<PH, PCGQ>) then reads only p.  Used in 3D, where the
+// fused pass A is fp64-issue-bound and its staged r / p_old / D^-1 / x rows
+// cost more issue slots than the extra pass costs bandwidth.
+__global__ void __launch_bounds__(kEwThreads)
+    pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old, double *p_new,
+             double *x, const lsg_pcg_scalars *scal) {
+  const int rhs = blockIdx.y;
+  const lsg_pcg_scalars &s = scal[rhs];
+  if (s.done != 0.0) return;
+  const double beta = s.beta, al = s.alpha;
+  const bool upd = s.first == 0.0;
+  const size_t off = (size_t)rhs * (size_t)n;
+  const int64_t stride = (int64_t)gridDim.x * kEwThreads;
+  for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
+    double R[4], P[4], D[4], X[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + u * stride;
+      if (t < n) {
+        R[u] = __ldg(r + off + t);
+        P[u] = __ldg(p_old + off + t);
+        D[u] = __ldg(dinv + t);
+        if (upd) X[u] = x[off + t];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + u * stride;
+      if (t < n) {
+        p_new[off + t] = fma(beta, P[u], R[u] * D[u]);
+        if (upd) x[off + t] = fma(al, P[u], X[u]);
       }
     }
   }
@@ -881,6 +921,16 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   return check_launch("zero_if_flag3d");
 }
 
+// LSG_PCG3D_FUSED=1 selects the fused single-kernel pass A (A/B measurements).
+static bool split_pass_a() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_PCG3D_FUSED");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const int64_t n = 3 * nodes_of(geo_of(op.grid));
   MArgs a = {};
@@ -900,7 +950,17 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     double *p_new = ws.parity ? ws.p : ws.p_alt;
     a.x2 = p_old;
     a.y2 = p_new;
-    int rc = dispatch<PCGA>(op, a, ws.k, st);
+    int rc;
+    if (split_pass_a()) {
+      pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_new, ws.x, ws.scal);
+      rc = check_launch("pcg_prep3d");
+      if (rc) return rc;
+      MArgs aq = a;
+      aq.x = p_new;
+      rc = dispatch<PCGQ>(op, aq, ws.k, st);
+    } else {
+      rc = dispatch<PCGA>(op, a, ws.k, st);
+    }
     if (rc) return rc;
     pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
     rc = check_launch("pcg_update3d");
