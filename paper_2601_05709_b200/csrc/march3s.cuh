@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   double *xchg = stage + Stage<PH, ACT>::doubles;                      // [2][kWarps][2*NOUT][32]
   uint32_t *stw = reinterpret_cast<uint32_t *>(xchg + Stage<PH, ACT>::xchg);  // [3][kWarps+1][32]
   __shared__ double scratch[NPA * kWarps];
+  __shared__ double wtab[16];  // per-tet weights (physics with kTable)
+  if constexpr (PH::kTable) ph.fill_table(wtab, threadIdx.x);
   auto SR = [&](int slot, int row, int s) -> double * {
     return stage + (((size_t)slot * (kWarps + 1) + row) * NS + s) * kRowSlot;
   };
@@ -324,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     if constexpr (ACT == SHAPE) {
       ph.cell(U, c.wc, own && (kk - 1) >= K0, C, part);
     } else {
-      ph.cell(U, c.wc, i, jw, kk - 1, C);
+      if constexpr (PH::kTable) ph.cell(U, c.wc, i, jw, kk - 1, C, wtab);
+      else ph.cell(U, c.wc, i, jw, kk - 1, C);
     }
     double T[4][NOUT];
 #pragma unroll

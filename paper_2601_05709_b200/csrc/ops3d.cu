@@ -63,6 +63,7 @@ __host__ __device__ constexpr int corner(int m, int v) {  // path vertex v of te
 // ---------------------------------------------------------------------------
 struct Elast {
   static constexpr int NIN = 3, NOUT = 3;
+  static constexpr bool kTable = false;
   double lam, mu, w0, w1;  // w(n) = w0 + w1 n = |T| (inside n + outside (4-n)) / 4
   double ih[3];
   __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 18) & 1u; }
@@ -124,8 +125,19 @@ struct Elast {
 // per cell than the general form above.
 struct ElastC {
   static constexpr int NIN = 3, NOUT = 3;
+  static constexpr bool kTable = true;  // per-CTA shared table of the tet weights
   double w0, w1;  // |T| (inside n + outside (4-n)) / 4 = w0 + w1 n
   double cs, cl;  // mu / h^2, lam / h^2
+
+  // tab[n] = w(n) mu/h^2, tab[8 + n] = w(n) lam/h^2 for n = 0..4; index 7
+  // (what invalid cells look up) gives 0
+  __device__ __forceinline__ void fill_table(double *tab, int t) const {
+    if (t < 16) {
+      const int n = t & 7;
+      const double w = n <= 4 ? fma((double)n, w1, w0) : 0.0;
+      tab[t] = w * (t < 8 ? cs : cl);
+    }
+  }
   __device__ __forceinline__ static bool valid(uint32_t w) { return Elast::valid(w); }
   __device__ __forceinline__ static uint32_t mask(uint32_t w) { return Elast::mask(w); }
 
@@ -140,11 +152,12 @@ struct ElastC {
   }
 
   template <int M>
-  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t word, double (*c)[NOUT]) const {
+  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t nbits, const double *tab,
+                                      double (*c)[NOUT]) const {
     constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
     constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
-    const double w = valid(word) ? fma((double)((word >> (3 * M)) & 7u), w1, w0) : 0.0;
-    const double s = w * cs, l = w * cl;
+    const uint32_t n = (nbits >> (3 * M)) & 7u;
+    const double s = tab[n], l = tab[8 + n];
     double D[3][3];  // D[axis][comp]
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -170,14 +183,16 @@ struct ElastC {
   }
 
   __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int, int, int,
-                                       double (*c)[NOUT]) const {
-    tet<0>(u, word, c); tet<1>(u, word, c); tet<2>(u, word, c);
-    tet<3>(u, word, c); tet<4>(u, word, c); tet<5>(u, word, c);
+                                       double (*c)[NOUT], const double *tab) const {
+    const uint32_t nb = valid(word) ? word : 0x3ffffu;  // invalid: every tet reads index 7
+    tet<0>(u, nb, tab, c); tet<1>(u, nb, tab, c); tet<2>(u, nb, tab, c);
+    tet<3>(u, nb, tab, c); tet<4>(u, nb, tab, c); tet<5>(u, nb, tab, c);
   }
 };
 
 struct H1 {
   static constexpr int NIN = 3, NOUT = 3;
+  static constexpr bool kTable = false;
   int nx, ny, nz;
   double m;          // mw |T| / 20
   double sw_t;       // sw |T|
@@ -257,6 +272,7 @@ struct H1 {
 template <int KB>
 struct Shape {
   static constexpr int NIN = 3 * KB, NOUT = 6;
+  static constexpr bool kTable = false;
   double lam, mu, vol_t, inv_volume, w0, w1;
   double ih[3];
   __device__ __forceinline__ static bool valid(uint32_t w) { return (w >> 18) & 1u; }
