@@ -184,6 +184,12 @@ int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream);
 int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol,
                   double maxiter, void *stream);
 int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream);
+/* Diagnostics of the PCG chunk graphs (lsg_pcg_iterate replays CUDA graphs):
+ * out4 = {cache hits, in-place updates, instantiations, host seconds spent
+ * capturing + updating/instantiating}.  LSG_NO_GRAPHS=1 in the environment
+ * launches the chunk kernels directly instead. */
+void lsg_graph_stats(double *out4);
+
 /* The update x += alpha p of iteration i is folded into pass A of iteration
  * i+1 (it reads p_i anyway), so a right-hand side that has just converged has
  * one update pending: call lsg_pcg_finish once after the last lsg_pcg_iterate,

@@ -79,6 +79,7 @@ SIGNATURES = {
     "lsg_pcg_start": (ctypes.c_int, [_O, _W, _D, _D, _D, _P]),
     "lsg_pcg_iterate": (ctypes.c_int, [_O, _W, _I, _P]),
     "lsg_pcg_finish": (ctypes.c_int, [_O, _W, _P]),
+    "lsg_graph_stats": (None, [_P]),
     "lsg_shape_rhs": (ctypes.c_int, [_O, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P]),
     "lsg_heat_shape": (ctypes.c_int, [_O, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
     "lsg_inverse_misfit": (ctypes.c_int, [_G, _I, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P, _P]),

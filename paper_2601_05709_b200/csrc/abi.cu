@@ -216,6 +216,10 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
   return pcg_iterate_graph(*op, *ws, niter, S(stream));
 }
 
+void lsg_graph_stats(double *out4) {
+  if (out4) graph_stats(out4);
+}
+
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream) {
   int rc = check_op(op);
   if (!rc) rc = check_ws(ws);

@@ -70,6 +70,7 @@ int mesh_elements(const lsg_grid &g, int32_t *conn, cudaStream_t st);
 int transport(const lsg_grid &g, const double *phi_in, const double *theta, double dt, int nsub,
               int smooth, double h, double *phi_out, double *tmp, cudaStream_t st);
 int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
+void graph_stats(double *out);
 
 namespace pg {  // the reference's own level-set scheme, 2D (pg2d.cu)
 int apply(const lsg_op &op, const double *x, double *y, cudaStream_t st);

@@ -37,6 +37,10 @@ def main():
         opt.step()
     torch.cuda.synchronize()
     fem.PCG_PROFILE = []
+    lib = _lib.load()
+    import ctypes
+    g0 = (ctypes.c_double * 4)()
+    lib.lsg_graph_stats(g0)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -44,6 +48,8 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     prof, fem.PCG_PROFILE = fem.PCG_PROFILE, None
+    g1 = (ctypes.c_double * 4)()
+    lib.lsg_graph_stats(g1)
     total = e0.elapsed_time(e1)
     out = {"config": args.config, "steps": args.steps, "ms_per_step": total / args.steps}
     for kind, name in ((_lib.LSG_OP_ELASTICITY, "state_pcg"), (_lib.LSG_OP_H1, "velocity_cg")):
@@ -54,6 +60,9 @@ def main():
                      "us_per_launched_iter": 1e3 * ms / max(launched, 1),
                      "rhs_iters_per_step": sum(p["rhs_iters"] for p in ch) / args.steps,
                      "chunks_per_step": len(ch) / args.steps}
+    out["graphs_per_step"] = dict(zip(("hits", "updates", "instantiations", "host_ms"),
+                                      [(b - a) / args.steps * (1e3 if i == 3 else 1)
+                                       for i, (a, b) in enumerate(zip(g0, g1))]))
     out["other_ms_per_step"] = out["ms_per_step"] - out["state_pcg"]["ms_per_step"] - out["velocity_cg"]["ms_per_step"]
     out["records"] = [{"cg_iters": list(r.cg_iters), "velocity_iters": r.velocity_iters,
                        "transport_substeps": r.transport_substeps, "reinit_substeps": r.reinit_substeps}
