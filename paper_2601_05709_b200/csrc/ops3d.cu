@@ -190,6 +190,7 @@ struct ElastC {
   }
 };
 
+struct H1;
 struct H1 {
   static constexpr int NIN = 3, NOUT = 3;
   static constexpr bool kTable = false;
@@ -269,6 +270,77 @@ struct H1 {
 };
 
 // Fused compliance + shape-derivative RHS for KB states at once.
+// The velocity form without the optional boundary-normal / frozen terms
+// (the BASELINE configs: mass + alpha vector Laplacian): per component the
+// six tets' stiffness fluxes k_a D_a with compile-time first-touch corners,
+// and the cell mass assembled per corner as m (n_v u_v + sum_{t ∋ v} s_t)
+// from the six tet sums s_t (n_v = 6 tets at corners 0 and 7, 2 elsewhere),
+// instead of the per-tet mass products of H1.
+struct H1P {
+  static constexpr int NIN = 3, NOUT = 3;
+  static constexpr bool kTable = false;
+  double m;      // mw |T| / 20
+  double ka[3];  // sw |T| / h_a^2
+  __device__ __forceinline__ static bool valid(uint32_t w) { return H1::valid(w); }
+  __device__ __forceinline__ static uint32_t mask(uint32_t w) { return H1::mask(w); }
+
+  static __host__ __device__ constexpr bool in_tet(int M, int v) {
+    return v == 0 || v == 7 || corner(M, 1) == v || corner(M, 2) == v;
+  }
+  static __host__ __device__ constexpr bool touched(int M, int v) {  // by a tet < M
+    return M > 0 && (in_tet(M - 1, v) || touched(M - 1, v));
+  }
+  template <int M, int V>
+  __device__ __forceinline__ static void put(double (*c)[NOUT], int q, double x) {
+    if constexpr (touched(M, V)) c[V][q] += x; else c[V][q] = x;
+  }
+  template <int M>
+  __device__ __forceinline__ void tet(const double (*u)[NIN], int q, double (*c)[NOUT],
+                                      double &st) const {
+    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
+    constexpr int P1 = corner(M, 1), P2 = corner(M, 2);
+    const double Fa = ka[a] * (u[P1][q] - u[0][q]);
+    const double Fb = ka[b] * (u[P2][q] - u[P1][q]);
+    const double Fc = ka[cc] * (u[7][q] - u[P2][q]);
+    put<M, 0>(c, q, -Fa);
+    put<M, P1>(c, q, Fa - Fb);
+    put<M, P2>(c, q, Fb - Fc);
+    put<M, 7>(c, q, Fc);
+    st = (u[0][q] + u[7][q]) + (u[P1][q] + u[P2][q]);
+  }
+  template <int V>
+  __device__ __forceinline__ void mass(const double (*u)[NIN], int q, const double (&S)[6],
+                                       double (*c)[NOUT]) const {
+    double sv = 0.0;
+    int nv = 0;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const bool in = (V == 0 || V == 7 || corner(t, 1) == V || corner(t, 2) == V);
+      if (in) { sv += S[t]; ++nv; }
+    }
+    c[V][q] = fma(m, fma((double)nv, u[V][q], sv), c[V][q]);
+  }
+
+  __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int, int, int,
+                                       double (*c)[NOUT]) const {
+    if (!valid(word)) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) c[v][q] = 0.0;
+      return;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double S[6];
+      tet<0>(u, q, c, S[0]); tet<1>(u, q, c, S[1]); tet<2>(u, q, c, S[2]);
+      tet<3>(u, q, c, S[3]); tet<4>(u, q, c, S[4]); tet<5>(u, q, c, S[5]);
+      mass<0>(u, q, S, c); mass<1>(u, q, S, c); mass<2>(u, q, S, c); mass<3>(u, q, S, c);
+      mass<4>(u, q, S, c); mass<5>(u, q, S, c); mass<6>(u, q, S, c); mass<7>(u, q, S, c);
+    }
+  }
+};
+
 template <int KB>
 struct Shape {
   static constexpr int NIN = 3 * KB, NOUT = 6;
@@ -836,6 +908,14 @@ static H1 make_h1(const Geo &g, const lsg_op &op) {
   return h;
 }
 
+static H1P make_h1_plain(const Geo &g, const lsg_op &op) {
+  H1P h;
+  const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+  h.m = op.p[0] * vol / 20.0;
+  for (int a = 0; a < 3; ++a) h.ka[a] = op.p[1] * vol * g.ih[a] * g.ih[a];
+  return h;
+}
+
 int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 
 static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
@@ -881,7 +961,10 @@ static int dispatch(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
     if (is_cubic(g)) return launch<ElastC, ACT>(make_elast_cubic(g, op), g, a, k, st);
     return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
   }
-  if (op.kind == LSG_OP_H1) return launch<H1, ACT>(make_h1(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_H1) {
+    if (op.p[2] == 0.0 && op.p[3] == 0.0) return launch<H1P, ACT>(make_h1_plain(g, op), g, a, k, st);
+    return launch<H1, ACT>(make_h1(g, op), g, a, k, st);
+  }
   set_error("unknown operator kind %d", op.kind);
   return LSG_ERR_ARG;
 }
