@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   const int li3 = (ic - lo) * 3;
   const int wbytes = (hi - lo + 1) * 24;
   const int64_t rown = (int64_t)jc * nxp + lo, rowu = (int64_t)jxc * nxp + lo;
+  const int64_t node_in_plane = (int64_t)jw * nxp + i;  // this lane's node within a plane
 
   // stage the window of node row n0.. (one plane) into ring slot `slot`
   auto stage_row = [&](int64_t n0, int slot, int srow) {
@@ -186,8 +187,9 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   };
   auto issue = [&](int kk, int slot) {
     if (kk <= kend) {
-      stage_row(kk * plane + rown, slot, w);
-      if (top) stage_row(kk * plane + rowu, slot, w + 1);
+      const int64_t kp = (int64_t)kk * plane;
+      stage_row(kp + rown, slot, w);
+      if (top) stage_row(kp + rowu, slot, w + 1);
     }
     cp_async_commit();
   };
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   auto prepare = [&](int kk, int slot, int srow, int64_t rowoff, bool ok, bool write_own, double *in,
                      double *raw, double *dg, uint32_t &wc) {
     wc = ok ? SW(slot, srow, lane) : 0u;
-    const uint32_t ph = (uint32_t)((kk * plane + rowoff) & 1);
+    const uint32_t ph = ((uint32_t)kk & (uint32_t)plane & 1u) ^ ((uint32_t)rowoff & 1u);
     auto V = [&](int s, int q) -> double {
       return SR(slot, srow, s)[(int)(ph ^ ((spm >> s) & 1u)) + li3 + q];
     };
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
           v[q] = fma(beta, po[q], v[q] * dg[q]);
         }
         if (write_own) {
-          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+          const int64_t node = (int64_t)kk * plane + node_in_plane;
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
             a.y2[voff + node * 3 + q] = v[q];
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   };
 
   auto emit = [&](int kk, uint32_t wc, const double *accv, const double *raw, const double *dg) {
-    const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
+    const int64_t node = (int64_t)kk * plane + node_in_plane;
     if constexpr (ACT == SHAPE) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
