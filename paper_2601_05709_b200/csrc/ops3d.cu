@@ -921,14 +921,27 @@ int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
   const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
   const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
-  // Short z-segments (one halo plane each): many CTAs in flight hide the
-  // per-plane latency of the serial march; at least ~4 waves when possible.
+  // z-segments (one halo plane each) sized for ~3 waves of CTAs and at most
+  // 32 planes (measured on cfg5: 16-32 planes, 3-4 waves are best; shorter
+  // segments pay more halo planes, one wave leaves a tail).
   const int64_t per_seg = nstrips * tiles * k;
   const int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  int64_t ns = ceil_div(4 * slots, per_seg);
+  static int waves = -1;  // LSG_M3_WAVES: target waves of CTAs (experiments)
+  if (waves < 0) {
+    const char *e = getenv("LSG_M3_WAVES");
+    waves = e ? atoi(e) : 3;
+    if (waves < 1) waves = 1;
+  }
+  int64_t ns = ceil_div(waves * slots, per_seg);
   if (ns < 1) ns = 1;
   int64_t s = ceil_div(g.nz + 1, ns);
-  if (s > 16) s = 16;
+  static int smax = -1;  // LSG_M3_SEGMAX: cap on planes per segment (experiments)
+  if (smax < 0) {
+    const char *e = getenv("LSG_M3_SEGMAX");
+    smax = e ? atoi(e) : 32;
+    if (smax < 6) smax = 6;
+  }
+  if (s > smax) s = smax;
   if (s < 6) s = 6;
   while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
   seg = (int)s;
