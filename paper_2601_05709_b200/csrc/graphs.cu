@@ -74,7 +74,7 @@ void graph_stats(double *out) {
 
 int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   if (niter <= 0) return LSG_OK;
-  if (graphs_off())
+  if (graphs_off() || (op.grid.dim == 2 && d2::pcg_persistent_ok(op, ws)))  // one launch already
     return (op.grid.dim == 2) ? d2::pcg_iterate(op, ws, niter, st) : d3::pcg_iterate(op, ws, niter, st);
   Key key;
   memset(&key, 0, sizeof(key));

@@ -286,19 +286,21 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 // processed.  Loads are branch-free: columns outside the grid load a clamped
 // (valid) address and get material word 0, so their cells contribute nothing.
 // ----------------------------------------------------------------------------
+// One marching task (strip group bx, row segment by, right-hand side rhs):
+// the body shared by the per-launch kernel below and the persistent PCG.
+// Adds this thread's reduction terms to part[].
 template <class PH, int ACT, class W>
-__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+__device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MArgs &a, int bx,
+                                           int by, int rhs, bool first, double beta,
+                                           double alpha_prev,
+                                           double (&part)[Traits<PH, ACT>::NP > 0 ? Traits<PH, ACT>::NP : 1]) {
   constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
-  constexpr int NP = Traits<PH, ACT>::NP;
-  constexpr int NPA = NP > 0 ? NP : 1;
   constexpr int NF = (ACT == SHAPE) ? NIN / NC : 1;  // fields read per node (SHAPE: states)
   constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
-  __shared__ double scratch[NPA * kWarps];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int strip = blockIdx.x * kWarps + warp;
-  const int rhs = blockIdx.z;
+  const int strip = bx * kWarps + warp;
   const W *words = static_cast<const W *>(a.words);
   const int nx = g.nx, ny = g.ny;
   const int64_t nxp = nx + 1;
@@ -308,51 +310,13 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
   const bool own = node_ok && lane >= 1 && lane <= kStrip;
   const int ic = min(max(i, 0), nx);  // clamped column: always a valid address
-  const int J0 = blockIdx.y * a.seg;
+  const int J0 = by * a.seg;
   const int J1 = min(J0 + a.seg, ny + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
-
-  double beta = 0.0, alpha_prev = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA) {
-    lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0 || a.finish_only) {  // uniform across the CTA
-      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      // converged: apply the pending x += alpha p of its last iteration
-      const double al = s.alpha;
-      if (own) {
-        for (int r = J0; r < J1; ++r) {
-          const int64_t node = (int64_t)r * nxp + i;
-          double xo[NC], po[NC];
-          ld_node<NC>(a.xs + voff, node, xo);
-          ld_node<NC>(a.x2 + voff, node, po);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) xo[c] = fma(al, po[c], xo[c]);
-          st_node<NC>(a.xs + voff, node, xo);
-        }
-      }
-      double d1[1] = {0.0}, t1[1];
-      const int nblk = gridDim.x * gridDim.y;
-      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk,
-                                         a.counters + rhs, blockIdx.y * gridDim.x + blockIdx.x,
-                                         nblk, scratch, t1))
-        if (threadIdx.x == 0) s.reserved[1] = 0.0;
-      return;
-    }
-    first = s.first != 0.0;
-    beta = s.beta;
-    alpha_prev = s.alpha;
-  } else if constexpr (ACT == RESID) {
-    if (a.scal[rhs].done != 0.0) return;
-  }
   const double *xin = a.x + voff + (size_t)ic * NC;
   const double *xin2 = (ACT == PCGA ? a.x2 + voff : a.x) + (size_t)ic * NC;
   const double *dvin = (HAS_DINV ? a.dinv : a.x) + (size_t)ic * NC;
   const W *win = words + ic;
-
-  double part[NPA];
-#pragma unroll
-  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
 
   struct Raw {
     double v[NF + (ACT == PCGA ? 1 : 0)][NC];
@@ -530,6 +494,67 @@ __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
     if (last_in_b) emit(ny, SB, accB);
     else emit(ny, SA, accA);
   }
+}
+
+template <class PH, int ACT, class W>
+__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+  constexpr int NC = PH::NC;  // components per node of each input field
+  constexpr int NP = Traits<PH, ACT>::NP;
+  constexpr int NPA = NP > 0 ? NP : 1;
+  __shared__ double scratch[NPA * kWarps];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = blockIdx.x * kWarps + warp;
+  const int rhs = blockIdx.z;
+  const int nx = g.nx, ny = g.ny;
+  const int64_t nxp = nx + 1;
+  const int64_t nn = nxp * (ny + 1);
+
+  const int i = strip * kStrip - 1 + lane;
+  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
+  const bool own = node_ok && lane >= 1 && lane <= kStrip;
+  const int ic = min(max(i, 0), nx);  // clamped column: always a valid address
+  const int J0 = blockIdx.y * a.seg;
+  const int J1 = min(J0 + a.seg, ny + 1);
+  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
+
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = false;
+  if constexpr (ACT == PCGA) {
+    lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0 || a.finish_only) {  // uniform across the CTA
+      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
+      // converged: apply the pending x += alpha p of its last iteration
+      const double al = s.alpha;
+      if (own) {
+        for (int r = J0; r < J1; ++r) {
+          const int64_t node = (int64_t)r * nxp + i;
+          double xo[NC], po[NC];
+          ld_node<NC>(a.xs + voff, node, xo);
+          ld_node<NC>(a.x2 + voff, node, po);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) xo[c] = fma(al, po[c], xo[c]);
+          st_node<NC>(a.xs + voff, node, xo);
+        }
+      }
+      double d1[1] = {0.0}, t1[1];
+      const int nblk = gridDim.x * gridDim.y;
+      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk,
+                                         a.counters + rhs, blockIdx.y * gridDim.x + blockIdx.x,
+                                         nblk, scratch, t1))
+        if (threadIdx.x == 0) s.reserved[1] = 0.0;
+      return;
+    }
+    first = s.first != 0.0;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  } else if constexpr (ACT == RESID) {
+    if (a.scal[rhs].done != 0.0) return;
+  }
+  double part[NPA];
+#pragma unroll
+  for (int t = 0; t < NPA; ++t) part[t] = 0.0;
+  march_core<PH, ACT, W>(ph, g, a, blockIdx.x, blockIdx.y, rhs, first, beta, alpha_prev, part);
 
   if constexpr (NP > 0) {
     const int nblk = gridDim.x * gridDim.y;

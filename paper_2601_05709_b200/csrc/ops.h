@@ -16,6 +16,7 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
               cudaStream_t st);
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st);
 int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st);
+bool pcg_persistent_ok(const lsg_op &op, const lsg_pcg_ws &ws);
 int shape_rhs(const lsg_op &op, int k, const double *u, double volume, double *vc, double *vv,
               double *out, double *partials, uint32_t *counter, cudaStream_t st);
 int heat_shape(const lsg_op &op, int k, const double *u, const double *weights, const double *fq,

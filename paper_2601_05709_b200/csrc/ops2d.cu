@@ -2,6 +2,9 @@
 // marching, see march2d.cuh), fused compliance + shape-derivative RHS,
 // velocity statistics, material words and the PCG update pass.
 #include <math.h>
+#include <stdlib.h>
+
+#include <cooperative_groups.h>
 
 #include "march2d_ops.cuh"
 #include "ops.h"
@@ -461,6 +464,229 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   return check_launch("zero_if_flag");
 }
 
+
+// ----------------------------------------------------------------------------
+// Persistent PCG (2D): all `niter` iterations of pass A + pass B in one
+// cooperative launch, two grid-wide barriers per iteration instead of two
+// kernel boundaries.  Every CTA keeps the per-RHS scalars in shared memory
+// and forms the alpha / beta reductions itself from the per-CTA partials in
+// one fixed order, so all CTAs take identical decisions (and the results are
+// deterministic); CTA 0 mirrors the scalars to global memory.  Same algorithm
+// and stopping rule as the two-kernel path (march<.., PCGA> + pcg_update).
+// ----------------------------------------------------------------------------
+namespace cgrp = cooperative_groups;
+
+template <class PH, int KMAX>
+__global__ void __launch_bounds__(kThreads)
+    pcg_persistent(PH ph, Geo g, MArgs a, int k, int tx, int ty, int niter, int parity0,
+                   double *p_even, double *p_odd, double *pbuf) {
+  constexpr int NC = PH::NC;
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double scratch[2 * KMAX * kWarps];
+  __shared__ double s_beta[KMAX], s_alpha[KMAX], s_rho[KMAX], s_atol[KMAX], s_iters[KMAX];
+  __shared__ double s_maxit[KMAX], s_pa[KMAX];
+  __shared__ int s_first[KMAX], s_done[KMAX], s_all;
+  const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
+  const int ncta = gridDim.x, cta = blockIdx.x;
+  double *pa = pbuf, *pb = pbuf + (size_t)ncta * KMAX;  // [ncta][KMAX], [ncta][2 KMAX]
+  if (threadIdx.x < KMAX) {
+    const int r = threadIdx.x;
+    const bool live = r < k;
+    const lsg_pcg_scalars &sc = a.scal[live ? r : 0];
+    s_beta[r] = sc.beta;
+    s_alpha[r] = sc.alpha;
+    s_rho[r] = sc.rho;
+    s_atol[r] = sc.atol;
+    s_iters[r] = sc.iters;
+    s_maxit[r] = sc.maxiter;
+    s_first[r] = sc.first != 0.0;
+    s_done[r] = live ? (sc.done != 0.0) : 1;
+  }
+  __syncthreads();
+  int parity = parity0;
+  const int ntask = tx * ty * k;
+  for (int it = 0; it < niter; ++it, parity ^= 1) {
+    if (threadIdx.x == 0) {
+      int all = 1;
+      for (int r = 0; r < KMAX; ++r) all &= s_done[r];
+      s_all = all;
+    }
+    __syncthreads();
+    if (s_all) continue;  // identical in every CTA: no barrier is skipped by only some
+    MArgs aa = a;
+    aa.x2 = parity ? p_odd : p_even;  // p_old
+    aa.y2 = parity ? p_even : p_odd;  // p_new
+    // pass A: p = M^-1 r + beta p_old, q = A p, p.q partials, pending x update
+    if (threadIdx.x < KMAX) s_pa[threadIdx.x] = 0.0;
+    __syncthreads();
+    for (int t = cta; t < ntask; t += ncta) {
+      const int rhs = t / (tx * ty), rem = t - rhs * (tx * ty);
+      if (s_done[rhs]) continue;
+      double part[1] = {0.0};
+      march_core<PH, PCGA, uint8_t>(ph, g, aa, rem % tx, rem / tx, rhs, s_first[rhs] != 0,
+                                   s_beta[rhs], s_alpha[rhs], part);
+      block_reduce<1, 0u>(part, scratch);
+      if (threadIdx.x == 0) s_pa[rhs] += part[0];
+      __syncthreads();
+    }
+    if (threadIdx.x < KMAX) pa[(size_t)cta * KMAX + threadIdx.x] = s_pa[threadIdx.x];
+    grid.sync();
+    {  // alpha = rho / p.q, all RHS in one fixed-order reduction (same in every CTA)
+      double acc[KMAX];
+#pragma unroll
+      for (int r = 0; r < KMAX; ++r) acc[r] = 0.0;
+      for (int c = threadIdx.x; c < ncta; c += kThreads)
+#pragma unroll
+        for (int r = 0; r < KMAX; ++r) acc[r] += __ldcg(pa + (size_t)c * KMAX + r);
+      block_reduce<KMAX, 0u>(acc, scratch);
+      if (threadIdx.x == 0) {
+        for (int r = 0; r < k; ++r) {
+          if (s_done[r]) continue;
+          s_alpha[r] = s_rho[r] / acc[r];
+          if (cta == 0) a.scal[r].pq = acc[r];
+        }
+      }
+      __syncthreads();
+    }
+    // pass B: r -= alpha q ; r.M^-1 r ; r.r
+    double part[2 * KMAX];
+#pragma unroll
+    for (int r = 0; r < 2 * KMAX; ++r) part[r] = 0.0;
+#pragma unroll
+    for (int r = 0; r < KMAX; ++r) {
+      if (r >= k || s_done[r]) continue;
+      const double alpha = s_alpha[r];
+      double *rv = const_cast<double *>(a.x) + (size_t)r * nn * NC;  // r (pass A reads it as x)
+      const double *qv = a.y + (size_t)r * nn * NC;
+      for (int64_t node = (int64_t)cta * kThreads + threadIdx.x; node < nn;
+           node += (int64_t)ncta * kThreads) {
+        double Q[NC], R[NC], D[NC];
+        ldg_node<NC>(qv, node, Q);
+        ldg_node<NC>(a.dinv, node, D);
+        ld_node<NC>(rv, node, R);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          R[c] = fma(-alpha, Q[c], R[c]);
+          part[2 * r] += R[c] * (R[c] * D[c]);
+          part[2 * r + 1] += R[c] * R[c];
+        }
+        st_node<NC>(rv, node, R);
+      }
+    }
+    block_reduce<2 * KMAX, 0u>(part, scratch);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int r = 0; r < 2 * KMAX; ++r) pb[(size_t)cta * 2 * KMAX + r] = part[r];
+    grid.sync();
+    {
+      double acc[2 * KMAX];
+#pragma unroll
+      for (int r = 0; r < 2 * KMAX; ++r) acc[r] = 0.0;
+      for (int c = threadIdx.x; c < ncta; c += kThreads)
+#pragma unroll
+        for (int r = 0; r < 2 * KMAX; ++r) acc[r] += __ldcg(pb + (size_t)c * 2 * KMAX + r);
+      block_reduce<2 * KMAX, 0u>(acc, scratch);
+      if (threadIdx.x == 0) {
+        for (int r = 0; r < k; ++r) {
+          if (s_done[r]) continue;
+          const double rz = acc[2 * r], rr = acc[2 * r + 1];
+          s_iters[r] += 1.0;
+          int done = 0;
+          if (sqrt(rr) < s_atol[r]) done = 1;
+          else if (s_iters[r] >= s_maxit[r]) done = 2;
+          else {
+            s_beta[r] = rz / s_rho[r];
+            s_rho[r] = rz;
+            s_first[r] = 0;
+          }
+          s_done[r] = done != 0;
+          if (cta == 0) {
+            lsg_pcg_scalars &sc = a.scal[r];
+            sc.iters = s_iters[r];
+            sc.rz_new = rz;
+            sc.rr = rr;
+            sc.reserved[1] = 1.0;  // x += alpha p of this iteration is pending
+            sc.alpha = s_alpha[r];
+            if (done) sc.done = (double)done;
+            else {
+              sc.beta = s_beta[r];
+              sc.rho = s_rho[r];
+              sc.first = 0.0;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// LSG_PCG2D_PERSISTENT=0 keeps the two-kernel (graph-replayed) iteration.
+static bool persistent_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_PCG2D_PERSISTENT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <class PH, int KMAX>
+static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws, int niter,
+                               cudaStream_t st) {
+  static int per_sm = -1;
+  if (per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent<PH, KMAX>, kThreads,
+                                                    0) != cudaSuccess)
+    per_sm = 0;
+  if (per_sm <= 0) return 1;  // not launchable cooperatively: caller falls back
+  static int ctas_march = -1;
+  if (ctas_march < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_march, march<PH, PCGA, uint8_t>,
+                                                    kThreads, 0) != cudaSuccess)
+    ctas_march = 4;
+  a.seg = seg_for(g, ws.k, ctas_march);
+  a.nstrips = nstrips_of(g);
+  const dim3 mg = march_grid(g, a.seg, ws.k);
+  const int ntask = (int)(mg.x * mg.y * ws.k);
+  // one task per CTA where possible, at least one CTA per SM for pass B
+  int ncta = ntask < kSMs ? kSMs : ntask;
+  if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
+  int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
+  double *pe = ws.p, *po = ws.p_alt, *pbuf = ws.partials;
+  PH phc = ph;
+  Geo gc = g;
+  void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &pe, &po, &pbuf};
+  if (cudaLaunchCooperativeKernel((void *)pcg_persistent<PH, KMAX>, dim3((unsigned)ncta),
+                                  dim3(kThreads), args, 0, st) != cudaSuccess)
+    return check_launch("pcg_persistent");
+  ws.parity ^= (niter & 1);
+  return check_launch("pcg_persistent");
+}
+
+template <class PH>
+static int launch_persistent(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws, int niter,
+                             cudaStream_t st) {
+  if (ws.k == 1) return launch_persistent_k<PH, 1>(ph, g, a, ws, niter, st);
+  if (ws.k <= 4) return launch_persistent_k<PH, 4>(ph, g, a, ws, niter, st);
+  return launch_persistent_k<PH, 8>(ph, g, a, ws, niter, st);
+}
+
+// Small systems only: there the two kernel boundaries per iteration dominate;
+// on large ones the work does and the grid barriers + cross-CTA reductions
+// would cost more than the launches they replace (cfg2: 112 vs 59 us).
+bool pcg_persistent_ok(const lsg_op &op, const lsg_pcg_ws &ws) {
+  static int64_t limit = -1;  // LSG_PCG2D_PERSIST_MAX: dofs x rhs threshold
+  if (limit < 0) {
+    const char *e = getenv("LSG_PCG2D_PERSIST_MAX");
+    limit = e ? atoll(e) : 600000;
+  }
+  if (!persistent_on() || ws.k > 8 || op.grid.dim != 2) return false;
+  if (op.kind != LSG_OP_ELASTICITY && op.kind != LSG_OP_H1 && op.kind != LSG_OP_LAPLACE) return false;
+  const int64_t nn = (int64_t)(op.grid.n[0] + 1) * (op.grid.n[1] + 1);
+  return nn * nc_of(op) * ws.k <= limit;
+}
+
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
@@ -473,6 +699,13 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   a.counters = ws.counters;
   a.dinv = ws.dinv;
   a.xs = ws.x;
+  if (pcg_persistent_ok(op, ws)) {
+    int rc = 1;
+    if (op.kind == LSG_OP_ELASTICITY) rc = launch_persistent<Elast>(make_elast(g, op), g, a, ws, niter, st);
+    else if (op.kind == LSG_OP_H1) rc = launch_persistent<H1>(make_h1(g, op), g, a, ws, niter, st);
+    else rc = launch_persistent<Lap>(make_lap(g, op), g, a, ws, niter, st);
+    if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = not cooperative, fall through
+  }
   const dim3 eg((unsigned)upd_blocks(nn, ws.k), (unsigned)ws.k);
   for (int it = 0; it < niter; ++it) {
     double *p_old = ws.parity ? ws.p_alt : ws.p;
