@@ -130,6 +130,8 @@ typedef struct {
   uint32_t *counters;
   double *p_alt;
   const double *dinv; /* n doubles: inverse Jacobi diagonal from lsg_inv_diag */
+  double *p_ring;     /* 2D: third direction buffer (k x n); x is updated every
+                         second iteration with two directions at once */
 } lsg_pcg_ws;
 
 int32_t lsg_abi_version(void);
@@ -190,10 +192,12 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
  * launches the chunk kernels directly instead. */
 void lsg_graph_stats(double *out4);
 
-/* The update x += alpha p of iteration i is folded into pass A of iteration
- * i+1 (it reads p_i anyway), so a right-hand side that has just converged has
- * one update pending: call lsg_pcg_finish once after the last lsg_pcg_iterate,
- * before reading x. */
+/* The updates x += alpha p are folded into pass A, which reads p anyway: in
+ * 3D that of iteration i into pass A of i+1; in 2D those of iterations i-2
+ * and i-1 into pass A of every even iteration i (directions rotate through
+ * p, p_alt, p_ring), which halves the x traffic.  A right-hand side that has
+ * just converged therefore has one or two updates pending: call
+ * lsg_pcg_finish once after the last lsg_pcg_iterate, before reading x. */
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream);
 
 /* Fused compliance evaluation + shape-derivative right-hand side --

@@ -67,6 +67,12 @@ bool graphs_off() {
 
 }  // namespace
 
+// 2D rotates three direction buffers (phase = iteration mod 3), 3D two
+void advance_parity(const lsg_op &op, lsg_pcg_ws &ws, int niter) {
+  if (op.grid.dim == 2) ws.parity = (ws.parity + niter) % 3;
+  else ws.parity ^= (niter & 1);
+}
+
 void graph_stats(double *out) {
   std::lock_guard<std::mutex> lock(g_mu);
   for (int i = 0; i < 4; ++i) out[i] = g_stats[i];
@@ -94,7 +100,7 @@ int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t 
       e.last_use = ++g_clock;
       g_stats[0] += 1;
       if (cudaGraphLaunch(e.exec, st) != cudaSuccess) return check_launch("graph launch");
-      ws.parity ^= (niter & 1);
+      advance_parity(op, ws, niter);
       return check_launch("graph launch");
     }
   }
@@ -126,7 +132,7 @@ int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t 
       g_stats[1] += 1;
       g_stats[3] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (cudaGraphLaunch(best->exec, st) != cudaSuccess) return check_launch("graph launch");
-      ws.parity ^= (niter & 1);
+      advance_parity(op, ws, niter);
       return check_launch("graph launch");
     }
     cudaGetLastError();  // clear the failed update; instantiate instead
@@ -146,7 +152,7 @@ int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t 
   }
   g_cache.push_back(Entry{key, shape, exec, ++g_clock});
   if (cudaGraphLaunch(exec, st) != cudaSuccess) return check_launch("graph launch");
-  ws.parity ^= (niter & 1);
+  advance_parity(op, ws, niter);
   return check_launch("graph launch");
 }
 

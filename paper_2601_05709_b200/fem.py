@@ -284,6 +284,7 @@ class _Workspace:
         self.p = torch.empty((k, n), **dev)
         self.q = torch.empty((k, n), **dev)
         self.p_alt = torch.empty((k, n), **dev)
+        self.p_ring = torch.empty((k, n), **dev)
         self.scal = torch.zeros((k, _lib.SCAL_DOUBLES), **dev)
         npart = int(_lib.load().lsg_partials_per_rhs(grid))
         self.partials = torch.zeros(k * npart * 4, **dev)
@@ -291,7 +292,7 @@ class _Workspace:
         self.host_scal = torch.zeros((k, _lib.SCAL_DOUBLES), dtype=torch.float64, pin_memory=True)
         self.ws = _lib.PcgWs()
         self.ws.k = k
-        for name in ("x", "b", "r", "p", "q", "scal", "partials", "counters", "p_alt"):
+        for name in ("x", "b", "r", "p", "q", "scal", "partials", "counters", "p_alt", "p_ring"):
             setattr(self.ws, name, getattr(self, name).data_ptr())
 
 

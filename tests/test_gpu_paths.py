@@ -1,0 +1,61 @@
+"""The three ways a 2D PCG chunk can run -- the persistent cooperative kernel
+(small systems), the CUDA-graph replay of the two-kernel iteration, and
+direct launches -- give the same solutions, including right-hand sides that
+converge in the middle of a chunk (their pending x updates are applied by the
+next pass A or by lsg_pcg_finish).  Each path runs in its own process because
+the switches are read once per process.  Needs a B200."""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, %(root)r)
+from paper_2601_05709_b200 import DirichletSet, ElasticityOperator, FunctionSpace, build_rect_mesh
+from paper_2601_05709_b200.fem import solve_batched
+mesh = build_rect_mesh((0.0, 0.0, 2.0, 1.0), 48, 24, [(1, lambda p: p[:, 0] < 1e-12)])
+space = FunctionSpace(mesh, 2)
+rng = np.random.default_rng(3)
+phi = torch.as_tensor(rng.standard_normal(mesh.num_vertices), device="cuda")
+op = ElasticityOperator(space, phi, (0.33, 0.38), 1e-3, DirichletSet.on_tags(space, 1))
+b = rng.standard_normal((3, space.dof_count))
+b[1] *= 1e-3          # converges at a different iteration
+b[2] = 0.0            # zero right-hand side: x = 0, no iterations
+bc = DirichletSet.on_tags(space, 1).dofs
+b[:, bc] = 0.0
+x, it = solve_batched(op, torch.as_tensor(b, device="cuda"), rtol=1e-10)
+np.save(sys.argv[1], x.cpu().numpy())
+print(json.dumps([int(v) for v in it.cpu()]))
+"""
+
+
+def run_path(tmp_path, name, env):
+    out = tmp_path / f"{name}.npy"
+    script = tmp_path / "solve.py"
+    script.write_text(SCRIPT % {"root": ROOT})
+    full = dict(os.environ, **env)
+    res = subprocess.run([sys.executable, str(script), str(out)], env=full, capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    return np.load(out), json.loads(res.stdout.strip().splitlines()[-1])
+
+
+def test_pcg_paths_agree(tmp_path):
+    xp, itp = run_path(tmp_path, "persistent", {})
+    xg, itg = run_path(tmp_path, "graph", {"LSG_PCG2D_PERSISTENT": "0"})
+    xd, itd = run_path(tmp_path, "direct", {"LSG_PCG2D_PERSISTENT": "0", "LSG_NO_GRAPHS": "1"})
+    assert itp[2] == itg[2] == itd[2] == 0 and not xp[2].any() and not xg[2].any()
+    assert itg == itd and np.array_equal(xg, xd)  # same kernels, same order: bitwise
+    for r in range(2):
+        assert itp[r] > 10 and abs(itp[r] - itg[r]) <= max(2, itp[r] // 20)
+        assert np.linalg.norm(xp[r] - xg[r]) <= 1e-8 * np.linalg.norm(xg[r])
