@@ -67,11 +67,8 @@ bool graphs_off() {
 
 }  // namespace
 
-// 2D rotates three direction buffers (phase = iteration mod 3), 3D two
-void advance_parity(const lsg_op &op, lsg_pcg_ws &ws, int niter) {
-  if (op.grid.dim == 2) ws.parity = (ws.parity + niter) % 3;
-  else ws.parity ^= (niter & 1);
-}
+// three direction buffers rotate (phase = iteration index mod 3)
+void advance_parity(const lsg_op &, lsg_pcg_ws &ws, int niter) { ws.parity = (ws.parity + niter) % 3; }
 
 void graph_stats(double *out) {
   std::lock_guard<std::mutex> lock(g_mu);

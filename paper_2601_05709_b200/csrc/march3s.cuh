@@ -103,13 +103,21 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     lsg_pcg_scalars &s = a.scal[rhs];
     if (s.done != 0.0 || a.finish_only) {  // CTA-uniform
       if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      const double al = s.alpha;  // pending x += alpha p of the last iteration
+      // converged after iteration L = iters - 1: alpha_L p_L and, for odd L,
+      // first alpha_{L-1} p_{L-1} are pending
+      const int L = (int)s.iters - 1;
+      const double al = s.alpha, al2 = s.reserved[2];
+      const bool two = s.reserved[1] > 1.5;
+      const double *pL = a.ring[L % 3] + voff, *pL1 = a.ring[(L + 2) % 3] + voff;
       if (own) {
         for (int kk = K0; kk < K1; ++kk) {
           const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            a.xs[voff + node * 3 + q] = fma(al, a.x2[voff + node * 3 + q], a.xs[voff + node * 3 + q]);
+          for (int q = 0; q < 3; ++q) {
+            double xv = a.xs[voff + node * 3 + q];
+            if (two) xv = fma(al2, pL1[node * 3 + q], xv);
+            a.xs[voff + node * 3 + q] = fma(al, pL[node * 3 + q], xv);
+          }
         }
       }
       double d1[1] = {0.0}, t1[1];

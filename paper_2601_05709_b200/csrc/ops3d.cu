@@ -442,7 +442,8 @@ struct MArgs {
   const double *x, *x2, *b;
   double *y, *y2;
   const double *dinv;
-  double *xs;  // PCGA: the iterate x (x += alpha_prev p_old is done in pass A)
+  double *xs;  // PCGA (finish): the iterate x
+  const double *ring[3];  // PCGA finish: the three direction buffers
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
@@ -476,6 +477,7 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
   } else if constexpr (ACT == PCGA || ACT == PCGQ) {
     lsg_pcg_scalars &s = a.scal[rhs];
     s.pq = tot[0];
+    s.reserved[2] = s.alpha;  // alpha_{i-1}, still pending on odd iterations
     s.alpha = s.rho / tot[0];
   } else if constexpr (ACT == STATS) {
     a.out[0] = tot[0];
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
       s.iters += 1.0;
       s.rz_new = tot[0];
       s.rr = tot[1];
-      s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending
+      s.reserved[1] = (((int)s.iters - 1) & 1) ? 2.0 : 1.0;  // pending x updates (as 2D)
       if (sqrt(tot[1]) < s.atol) s.done = 1.0;
       else if (s.iters >= s.maxiter) s.done = 2.0;
       else {
@@ -556,22 +558,24 @@ __global__ void __launch_bounds__(kEwThreads, 4)
 }
 
 // Split pass A, first half (elementwise, HBM-bound): p = D^-1 r + beta p_old
-// and the pending x += alpha_prev p_old of the previous iteration.  The
-// stencil half (march3s<PH, PCGQ>) then reads only p.  Used in 3D, where the
-// fused pass A is fp64-issue-bound and its staged r / p_old / D^-1 / x rows
-// cost more issue slots than the extra pass costs bandwidth.
+// and, on even iterations i >= 2, the two pending x updates of iterations i-2
+// and i-1 (three direction buffers rotate, so p_{i-2} is still there: x is
+// read and written every second iteration only).  The stencil half
+// (march3s<PH, PCGQ>) then reads only p.  Used in 3D, where a fused pass A is
+// fp64-issue-bound.
 __global__ void __launch_bounds__(kEwThreads)
-    pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old, double *p_new,
-             double *x, const lsg_pcg_scalars *scal) {
+    pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old,
+             const double *p_old2, double *p_new, double *x, const lsg_pcg_scalars *scal) {
   const int rhs = blockIdx.y;
   const lsg_pcg_scalars &s = scal[rhs];
   if (s.done != 0.0) return;
-  const double beta = s.beta, al = s.alpha;
-  const bool upd = s.first == 0.0;
+  const double beta = s.beta, al = s.alpha, al2 = s.reserved[2];
+  const int it = (int)s.iters;
+  const bool upd = it >= 2 && (it & 1) == 0;
   const size_t off = (size_t)rhs * (size_t)n;
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
-    double R[4], P[4], D[4], X[4];
+    double R[4], P[4], D[4], X[4], P2[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t t = base + u * stride;
@@ -579,7 +583,10 @@ __global__ void __launch_bounds__(kEwThreads)
         R[u] = __ldg(r + off + t);
         P[u] = __ldg(p_old + off + t);
         D[u] = __ldg(dinv + t);
-        if (upd) X[u] = x[off + t];
+        if (upd) {
+          X[u] = x[off + t];
+          P2[u] = __ldg(p_old2 + off + t);
+        }
       }
     }
 #pragma unroll
@@ -587,7 +594,7 @@ __global__ void __launch_bounds__(kEwThreads)
       const int64_t t = base + u * stride;
       if (t < n) {
         p_new[off + t] = fma(beta, P[u], R[u] * D[u]);
-        if (upd) x[off + t] = fma(al, P[u], X[u]);
+        if (upd) x[off + t] = fma(al, P[u], fma(al2, P2[u], X[u]));
       }
     }
   }
@@ -1026,30 +1033,18 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   a.counters = ws.counters;
   rc = dispatch<RESID>(op, a, ws.k, st);
   if (rc) return rc;
-  // the first pass A reads p_old = ws.p with beta = 0: it must be finite
-  if (cudaMemsetAsync(ws.p, 0, sizeof(double) * (size_t)n * ws.k, st) != cudaSuccess)
+  // the first pass A reads p_old = ring[2] = ws.p_ring with beta = 0: it must be finite
+  if (cudaMemsetAsync(ws.p_ring, 0, sizeof(double) * (size_t)n * ws.k, st) != cudaSuccess)
     return check_launch("pcg_start3d memset");
   zero_if_flag<<<dim3(64, ws.k), 256, 0, st>>>(n, ws.scal, ws.x);
   return check_launch("zero_if_flag3d");
 }
 
-// LSG_PCG3D_FUSED=1 selects the fused single-kernel pass A (A/B measurements).
-static bool split_pass_a() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("LSG_PCG3D_FUSED");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const int64_t n = 3 * nodes_of(geo_of(op.grid));
   MArgs a = {};
-  a.x = ws.r;
   a.y = ws.q;
   a.dinv = ws.dinv;
-  a.xs = ws.x;
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
@@ -1057,27 +1052,21 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   int64_t slots = (int64_t)kSMs * 4 / ws.k;
   if (slots < 1) slots = 1;
   const dim3 eg((unsigned)(need < slots ? need : slots), (unsigned)ws.k);
+  double *const ring[3] = {ws.p, ws.p_alt, ws.p_ring};
   for (int it = 0; it < niter; ++it) {
-    double *p_old = ws.parity ? ws.p_alt : ws.p;
-    double *p_new = ws.parity ? ws.p : ws.p_alt;
-    a.x2 = p_old;
-    a.y2 = p_new;
-    int rc;
-    if (split_pass_a()) {
-      pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_new, ws.x, ws.scal);
-      rc = check_launch("pcg_prep3d");
-      if (rc) return rc;
-      MArgs aq = a;
-      aq.x = p_new;
-      rc = dispatch<PCGQ>(op, aq, ws.k, st);
-    } else {
-      rc = dispatch<PCGA>(op, a, ws.k, st);
-    }
+    const int ph = ws.parity;  // iteration index mod 3 = slot of the new direction
+    double *p_new = ring[ph], *p_old = ring[ph == 0 ? 2 : ph - 1];
+    double *p_old2 = ring[ph == 2 ? 0 : ph + 1];
+    pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_old2, p_new, ws.x, ws.scal);
+    int rc = check_launch("pcg_prep3d");
+    if (rc) return rc;
+    a.x = p_new;
+    rc = dispatch<PCGQ>(op, a, ws.k, st);
     if (rc) return rc;
     pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
     rc = check_launch("pcg_update3d");
     if (rc) return rc;
-    ws.parity ^= 1;
+    ws.parity = ph == 2 ? 0 : ph + 1;
   }
   return LSG_OK;
 }
@@ -1085,7 +1074,9 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
 int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
   MArgs a = {};
   a.x = ws.r;
-  a.x2 = ws.parity ? ws.p_alt : ws.p;
+  a.ring[0] = ws.p;
+  a.ring[1] = ws.p_alt;
+  a.ring[2] = ws.p_ring;
   a.dinv = ws.dinv;
   a.xs = ws.x;
   a.scal = ws.scal;
