@@ -504,7 +504,7 @@ namespace d3 {
 // ---------------------------------------------------------------------------
 // Elementwise kernels
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kEwThreads, 4)
+__global__ void __launch_bounds__(kEwThreads)
     pcg_update(int64_t n, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
                double *partials, uint32_t *counters) {
   __shared__ double scratch[2 * (kEwThreads / 32)];
@@ -1048,8 +1048,14 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
+  static int ew = -1;  // LSG_EW_CTAS: elementwise CTAs per SM (experiments)
+  if (ew < 0) {
+    const char *e = getenv("LSG_EW_CTAS");
+    ew = e ? atoi(e) : 4;
+    if (ew < 1) ew = 1;
+  }
   int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
-  int64_t slots = (int64_t)kSMs * 4 / ws.k;
+  int64_t slots = (int64_t)kSMs * ew / ws.k;
   if (slots < 1) slots = 1;
   const dim3 eg((unsigned)(need < slots ? need : slots), (unsigned)ws.k);
   double *const ring[3] = {ws.p, ws.p_alt, ws.p_ring};
