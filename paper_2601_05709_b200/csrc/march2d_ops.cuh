@@ -505,7 +505,10 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
 }
 
 template <class PH, int ACT, class W>
-__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+#ifndef LSG_M2_MINB
+#define LSG_M2_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, LSG_M2_MINB) march(PH ph, Geo g, MArgs a) {
   constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NP = Traits<PH, ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
