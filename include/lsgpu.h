@@ -130,7 +130,7 @@ typedef struct {
   uint32_t *counters;
   double *p_alt;
   const double *dinv; /* n doubles: inverse Jacobi diagonal from lsg_inv_diag */
-  double *p_ring;     /* 2D: third direction buffer (k x n); x is updated every
+  double *p_ring;     /* 3D: third direction buffer (k x n); x is updated every
                          second iteration with two directions at once */
 } lsg_pcg_ws;
 
@@ -193,11 +193,12 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
 void lsg_graph_stats(double *out4);
 
 /* The updates x += alpha p are folded into pass A, which reads p anyway: in
- * 3D that of iteration i into pass A of i+1; in 2D those of iterations i-2
- * and i-1 into pass A of every even iteration i (directions rotate through
- * p, p_alt, p_ring), which halves the x traffic.  A right-hand side that has
- * just converged therefore has one or two updates pending: call
- * lsg_pcg_finish once after the last lsg_pcg_iterate, before reading x. */
+ * 2D that of iteration i into pass A of i+1; in 3D those of iterations i-2
+ * and i-1 into the elementwise half of pass A of every even iteration i
+ * (directions rotate through p, p_alt, p_ring), which halves the x traffic.
+ * A right-hand side that has just converged therefore has one or two updates
+ * pending: call lsg_pcg_finish once after the last lsg_pcg_iterate, before
+ * reading x. */
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream);
 
 /* Fused compliance evaluation + shape-derivative right-hand side --

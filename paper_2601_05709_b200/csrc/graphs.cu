@@ -67,8 +67,11 @@ bool graphs_off() {
 
 }  // namespace
 
-// three direction buffers rotate (phase = iteration index mod 3)
-void advance_parity(const lsg_op &, lsg_pcg_ws &ws, int niter) { ws.parity = (ws.parity + niter) % 3; }
+// 3D rotates three direction buffers (phase = iteration index mod 3), 2D two
+void advance_parity(const lsg_op &op, lsg_pcg_ws &ws, int niter) {
+  if (op.grid.dim == 3) ws.parity = (ws.parity + niter) % 3;
+  else ws.parity ^= (niter & 1);
+}
 
 void graph_stats(double *out) {
   std::lock_guard<std::mutex> lock(g_mu);

@@ -18,9 +18,7 @@ struct MArgs {
   double *y;           // APPLY: y ; RESID: r ; PCGA: q ; SHAPE: vec_cost
   double *y2;          // PCGA: p (written) ; SHAPE: vec_vol
   const double *dinv;  // RESID / PCGA: inverse Jacobi diagonal (1 on Dirichlet dofs)
-  double *xs;          // PCGA: the iterate x (its pending updates are applied here)
-  const double *x3;    // PCGA: p of two iterations ago (even iterations)
-  const double *ring[3];  // PCGA finish: the three direction buffers
+  double *xs;          // PCGA: the iterate x (x += alpha_prev p_old is done here)
   int finish_only;     // PCGA: only apply pending x updates of converged rhs
   lsg_pcg_scalars *scal;
   double *partials;
@@ -264,7 +262,6 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
   } else if constexpr (ACT == PCGA) {
     lsg_pcg_scalars &s = a.scal[rhs];
     s.pq = tot[0];
-    s.reserved[2] = s.alpha;  // alpha_{i-1}, still pending on odd iterations
     s.alpha = s.rho / tot[0];
   } else if constexpr (ACT == STATS) {
     a.out[0] = tot[0];
@@ -295,7 +292,7 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 template <class PH, int ACT, class W>
 __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MArgs &a, int bx,
                                            int by, int rhs, bool first, double beta,
-                                           double alpha_prev, double alpha_prev2, bool upd_x,
+                                           double alpha_prev,
                                            double (&part)[Traits<PH, ACT>::NP > 0 ? Traits<PH, ACT>::NP : 1]) {
   constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
@@ -324,8 +321,7 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
   struct Raw {
     double v[NF + (ACT == PCGA ? 1 : 0)][NC];
     double dv[NC];
-    double xv[NC];  // PCGA: x of an owned node (updated on even iterations)
-    double p2[NC];  // PCGA: p_{i-2} of an owned node (even iterations)
+    double xv[NC];  // PCGA: x of an owned node (updated with the previous alpha)
     uint32_t wc;
   };
   struct Row {
@@ -348,10 +344,7 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
         } else {
           ldg_node<NC>(xin2, off, f.v[1]);
         }
-        if (upd_x && own && r >= J0 && r < J1) {
-          ld_node<NC>(a.xs + voff, off + i, f.xv);
-          ldg_node<NC>(a.x3 + voff, off + i, f.p2);
-        }
+        if (!first && own && r >= J0 && r < J1) ld_node<NC>(a.xs + voff, off + i, f.xv);
       }
       if constexpr (HAS_DINV) ldg_node<NC>(dvin, off, f.dv);
     }
@@ -381,11 +374,10 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
         if (own && r >= J0 && r < J1) {
           const int64_t node = (int64_t)r * nxp + i;
           st_node<NC>(a.y2 + voff, node, v);
-          if (upd_x) {  // x_i = (x_{i-2} + alpha_{i-2} p_{i-2}) + alpha_{i-1} p_{i-1}
+          if (!first) {  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
             double xn[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-              xn[c] = fma(alpha_prev, f.v[1][c], fma(alpha_prev2, f.p2[c], f.xv[c]));
+            for (int c = 0; c < NC; ++c) xn[c] = fma(alpha_prev, f.v[1][c], f.xv[c]);
             st_node<NC>(a.xs + voff, node, xn);
           }
         }
@@ -505,10 +497,7 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
 }
 
 template <class PH, int ACT, class W>
-#ifndef LSG_M2_MINB
-#define LSG_M2_MINB 1
-#endif
-__global__ void __launch_bounds__(kThreads, LSG_M2_MINB) march(PH ph, Geo g, MArgs a) {
+__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NP = Traits<PH, ACT>::NP;
   constexpr int NPA = NP > 0 ? NP : 1;
@@ -529,31 +518,22 @@ __global__ void __launch_bounds__(kThreads, LSG_M2_MINB) march(PH ph, Geo g, MAr
   const int J1 = min(J0 + a.seg, ny + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
 
-  double beta = 0.0, alpha_prev = 0.0, alpha_prev2 = 0.0;
-  bool first = false, upd_x = false;
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = false;
   if constexpr (ACT == PCGA) {
     lsg_pcg_scalars &s = a.scal[rhs];
     if (s.done != 0.0 || a.finish_only) {  // uniform across the CTA
       if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      // converged after iteration L = iters - 1: apply its pending updates,
-      // alpha_L p_L and, for odd L, first alpha_{L-1} p_{L-1}
-      const int L = (int)s.iters - 1;
-      const double al = s.alpha, al2 = s.reserved[2];
-      const bool two = s.reserved[1] > 1.5;
-      const double *pL = a.ring[L % 3] + voff;
-      const double *pL1 = a.ring[(L + 2) % 3] + voff;
+      // converged: apply the pending x += alpha p of its last iteration
+      const double al = s.alpha;
       if (own) {
         for (int r = J0; r < J1; ++r) {
           const int64_t node = (int64_t)r * nxp + i;
-          double xo[NC], po[NC], po2[NC];
+          double xo[NC], po[NC];
           ld_node<NC>(a.xs + voff, node, xo);
-          ld_node<NC>(pL, node, po);
-          if (two) ld_node<NC>(pL1, node, po2);
+          ld_node<NC>(a.x2 + voff, node, po);
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            if (two) xo[c] = fma(al2, po2[c], xo[c]);
-            xo[c] = fma(al, po[c], xo[c]);
-          }
+          for (int c = 0; c < NC; ++c) xo[c] = fma(al, po[c], xo[c]);
           st_node<NC>(a.xs + voff, node, xo);
         }
       }
@@ -568,17 +548,13 @@ __global__ void __launch_bounds__(kThreads, LSG_M2_MINB) march(PH ph, Geo g, MAr
     first = s.first != 0.0;
     beta = s.beta;
     alpha_prev = s.alpha;
-    alpha_prev2 = s.reserved[2];
-    const int it = (int)s.iters;  // this is iteration `it` of the solve
-    upd_x = it >= 2 && (it & 1) == 0;
   } else if constexpr (ACT == RESID) {
     if (a.scal[rhs].done != 0.0) return;
   }
   double part[NPA];
 #pragma unroll
   for (int t = 0; t < NPA; ++t) part[t] = 0.0;
-  march_core<PH, ACT, W>(ph, g, a, blockIdx.x, blockIdx.y, rhs, first, beta, alpha_prev,
-                         alpha_prev2, upd_x, part);
+  march_core<PH, ACT, W>(ph, g, a, blockIdx.x, blockIdx.y, rhs, first, beta, alpha_prev, part);
 
   if constexpr (NP > 0) {
     const int nblk = gridDim.x * gridDim.y;

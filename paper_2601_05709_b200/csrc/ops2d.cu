@@ -69,10 +69,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
       s.iters += 1.0;
       s.rz_new = tot[0];
       s.rr = tot[1];
-      // pending x updates after iteration L = iters - 1 (applied by the pass A of
-      // the next even iteration, or by lsg_pcg_finish): L even -> alpha_L p_L;
-      // L odd -> alpha_{L-1} p_{L-1} and alpha_L p_L
-      s.reserved[1] = (((int)s.iters - 1) & 1) ? 2.0 : 1.0;
+      s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending (next pass A / finish)
       if (sqrt(tot[1]) < s.atol) {
         s.done = 1.0;
       } else if (s.iters >= s.maxiter) {
@@ -482,12 +479,11 @@ namespace cgrp = cooperative_groups;
 template <class PH, int KMAX>
 __global__ void __launch_bounds__(kThreads)
     pcg_persistent(PH ph, Geo g, MArgs a, int k, int tx, int ty, int niter, int parity0,
-                   double *ring0, double *ring1, double *ring2, double *pbuf) {
+                   double *p_even, double *p_odd, double *pbuf) {
   constexpr int NC = PH::NC;
   cgrp::grid_group grid = cgrp::this_grid();
-  double *const ring[3] = {ring0, ring1, ring2};
   __shared__ double scratch[2 * KMAX * kWarps];
-  __shared__ double s_beta[KMAX], s_alpha[KMAX], s_alpha2[KMAX], s_rho[KMAX], s_atol[KMAX], s_iters[KMAX];
+  __shared__ double s_beta[KMAX], s_alpha[KMAX], s_rho[KMAX], s_atol[KMAX], s_iters[KMAX];
   __shared__ double s_maxit[KMAX], s_pa[KMAX];
   __shared__ int s_first[KMAX], s_done[KMAX], s_all;
   const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
@@ -499,7 +495,6 @@ __global__ void __launch_bounds__(kThreads)
     const lsg_pcg_scalars &sc = a.scal[live ? r : 0];
     s_beta[r] = sc.beta;
     s_alpha[r] = sc.alpha;
-    s_alpha2[r] = sc.reserved[2];
     s_rho[r] = sc.rho;
     s_atol[r] = sc.atol;
     s_iters[r] = sc.iters;
@@ -508,9 +503,9 @@ __global__ void __launch_bounds__(kThreads)
     s_done[r] = live ? (sc.done != 0.0) : 1;
   }
   __syncthreads();
-  int phase = parity0;  // iteration index mod 3 = slot of the new direction
+  int parity = parity0;
   const int ntask = tx * ty * k;
-  for (int it = 0; it < niter; ++it, phase = (phase == 2 ? 0 : phase + 1)) {
+  for (int it = 0; it < niter; ++it, parity ^= 1) {
     if (threadIdx.x == 0) {
       int all = 1;
       for (int r = 0; r < KMAX; ++r) all &= s_done[r];
@@ -519,9 +514,8 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     if (s_all) continue;  // identical in every CTA: no barrier is skipped by only some
     MArgs aa = a;
-    aa.y2 = ring[phase];                          // p_i
-    aa.x2 = ring[phase == 0 ? 2 : phase - 1];     // p_{i-1}
-    aa.x3 = ring[phase == 2 ? 0 : phase + 1];     // p_{i-2}
+    aa.x2 = parity ? p_odd : p_even;  // p_old
+    aa.y2 = parity ? p_even : p_odd;  // p_new
     // pass A: p = M^-1 r + beta p_old, q = A p, p.q partials, pending x update
     if (threadIdx.x < KMAX) s_pa[threadIdx.x] = 0.0;
     __syncthreads();
@@ -529,10 +523,8 @@ __global__ void __launch_bounds__(kThreads)
       const int rhs = t / (tx * ty), rem = t - rhs * (tx * ty);
       if (s_done[rhs]) continue;
       double part[1] = {0.0};
-      const int itr = (int)s_iters[rhs];
       march_core<PH, PCGA, uint8_t>(ph, g, aa, rem % tx, rem / tx, rhs, s_first[rhs] != 0,
-                                   s_beta[rhs], s_alpha[rhs], s_alpha2[rhs],
-                                   itr >= 2 && (itr & 1) == 0, part);
+                                   s_beta[rhs], s_alpha[rhs], part);
       block_reduce<1, 0u>(part, scratch);
       if (threadIdx.x == 0) s_pa[rhs] += part[0];
       __syncthreads();
@@ -550,7 +542,6 @@ __global__ void __launch_bounds__(kThreads)
       if (threadIdx.x == 0) {
         for (int r = 0; r < k; ++r) {
           if (s_done[r]) continue;
-          s_alpha2[r] = s_alpha[r];
           s_alpha[r] = s_rho[r] / acc[r];
           if (cta == 0) a.scal[r].pq = acc[r];
         }
@@ -614,8 +605,7 @@ __global__ void __launch_bounds__(kThreads)
             sc.iters = s_iters[r];
             sc.rz_new = rz;
             sc.rr = rr;
-            sc.reserved[1] = (((int)s_iters[r] - 1) & 1) ? 2.0 : 1.0;  // pending x updates
-            sc.reserved[2] = s_alpha2[r];
+            sc.reserved[1] = 1.0;  // x += alpha p of this iteration is pending
             sc.alpha = s_alpha[r];
             if (done) sc.done = (double)done;
             else {
@@ -663,14 +653,14 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
   int ncta = ntask < kSMs ? kSMs : ntask;
   if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
   int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
-  double *r0 = ws.p, *r1 = ws.p_alt, *r2 = ws.p_ring, *pbuf = ws.partials;
+  double *pe = ws.p, *po = ws.p_alt, *pbuf = ws.partials;
   PH phc = ph;
   Geo gc = g;
-  void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &r0, &r1, &r2, &pbuf};
+  void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &pe, &po, &pbuf};
   if (cudaLaunchCooperativeKernel((void *)pcg_persistent<PH, KMAX>, dim3((unsigned)ncta),
                                   dim3(kThreads), args, 0, st) != cudaSuccess)
     return check_launch("pcg_persistent");
-  ws.parity = (ws.parity + niter) % 3;
+  ws.parity ^= (niter & 1);
   return check_launch("pcg_persistent");
 }
 
@@ -717,17 +707,11 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = not cooperative, fall through
   }
   const dim3 eg((unsigned)upd_blocks(nn, ws.k), (unsigned)ws.k);
-  double *const ring[3] = {ws.p, ws.p_alt, ws.p_ring};
-  // a right-hand side that converges inside the chunk applies its pending x
-  // updates in the next pass A launch (finish path), which needs the ring
-  a.ring[0] = ws.p;
-  a.ring[1] = ws.p_alt;
-  a.ring[2] = ws.p_ring;
   for (int it = 0; it < niter; ++it) {
-    const int ph = ws.parity;  // iteration index mod 3 = slot of the new direction
-    a.y2 = ring[ph];                    // p_i
-    a.x2 = ring[ph == 0 ? 2 : ph - 1];  // p_{i-1}
-    a.x3 = ring[ph == 2 ? 0 : ph + 1];  // p_{i-2}
+    double *p_old = ws.parity ? ws.p_alt : ws.p;
+    double *p_new = ws.parity ? ws.p : ws.p_alt;
+    a.x2 = p_old;
+    a.y2 = p_new;
     int rc = dispatch_op<PCGA>(op, a, ws.k, st);
     if (rc) return rc;
     if (nc_of(op) == 1)
@@ -738,7 +722,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
                                                ws.counters);
     rc = check_launch("pcg_update2d");
     if (rc) return rc;
-    ws.parity = ph == 2 ? 0 : ph + 1;
+    ws.parity ^= 1;
   }
   return LSG_OK;
 }
@@ -749,9 +733,7 @@ int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
   MArgs a = {};
   a.words = op.words;
   a.x = ws.r;
-  a.ring[0] = ws.p;
-  a.ring[1] = ws.p_alt;
-  a.ring[2] = ws.p_ring;
+  a.x2 = ws.parity ? ws.p_alt : ws.p;
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
