@@ -344,11 +344,11 @@ def b200_arm(args, world, rank, local):
                                                    "Jacobi + r.z, r.r)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(),
-                         "traffic_note": "DRAM bytes of one (even) PCG iteration, pass A + pass B, "
-                                         "from profiles/r01_ncu_pcg.json (cold cache); below the "
-                                         "algorithmic count: the x updates are folded into pass A "
-                                         "and done every second iteration (8.5 of the canonical "
-                                         "10 vectors on average) and some writes stay in L2",
+                         "traffic_note": "DRAM bytes of one PCG iteration, pass A + pass B, from "
+                                         "profiles/r01_ncu_pcg.json (cold cache); below the "
+                                         "algorithmic count because x += alpha p is folded into "
+                                         "pass A (9 of the canonical 10 vectors) and some writes "
+                                         "stay in L2",
                          "peak_kind": peak_kind,
                          "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration",
                          "pcg_ms_in_timed_region": pcg_ms, "pcg_share_of_step": all_ms / (t_local * 1e3),
