@@ -14,7 +14,8 @@ HEADER = os.path.join(ROOT, "include", "lsgpu.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char \*)\s*\**(lsg_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void|const char \*)\s*\**(lsg_\w+)\(",
+                                 text, re.M)))
 
 
 def test_library_present():
@@ -51,3 +52,39 @@ def test_product_refuses_cpu():
         pytest.skip("GPU present")
     with pytest.raises(_lib.NativeUnavailable):
         _lib.load()
+
+
+def _op(kind, dim=2, words=1):
+    n = (8, 4) if dim == 2 else (4, 3, 2)
+    lo, hi = (0.0,) * dim, (2.0, 1.0, 1.0)[:dim]
+    op = _lib.Op()
+    op.kind = kind
+    op.grid = _lib.make_grid(dim, n, lo, hi)
+    op.words = words or None  # never dereferenced: validation fails first
+    for i in range(4):
+        op.p[i] = 1.0
+    return op
+
+
+def test_argument_errors_are_reported_before_any_device_work():
+    """The C ABI validates its arguments on the host and reports LSG_ERR_ARG with a
+    message (ConfigError on the Python side), without touching the device."""
+    lib = _lib.load(require_device=False)
+    null = ctypes.c_void_p(None)
+    cases = [
+        (lambda: lib.lsg_apply(None, 1, null, null, null), b"null operator"),
+        (lambda: lib.lsg_apply(_op(99), 1, null, null, null), b"unknown operator kind"),
+        (lambda: lib.lsg_apply(_op(_lib.LSG_OP_ELASTICITY, words=0), 1, null, null, null),
+         b"words missing"),
+        (lambda: lib.lsg_apply(_op(_lib.LSG_OP_LAPLACE, dim=3), 1, null, null, null), b"2D only"),
+        (lambda: lib.lsg_heat_shape(_op(_lib.LSG_OP_ELASTICITY), 1, null, null, null, null, 1.0,
+                                    null, null, null, null, null, null), b"scalar diffusion"),
+        (lambda: lib.lsg_shape_rhs(_op(_lib.LSG_OP_ELASTICITY), 1, null, 0.0, null, null, null,
+                                   null, null, null, null), b"volume"),
+        (lambda: lib.lsg_inverse_misfit(_lib.make_grid(3, (2, 2, 2), (0, 0, 0), (1, 1, 1)), 1, null,
+                                        null, null, null, null, 1.0, 1.0, null, null, null, null,
+                                        null, null), b"2D only"),
+    ]
+    for fn, msg in cases:
+        assert fn() == _lib.LSG_ERR_ARG
+        assert msg in lib.lsg_last_error(), (msg, lib.lsg_last_error())
