@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kEwThreads)
 // read and written every second iteration only).  The stencil half
 // (march3s<PH, PCGQ>) then reads only p.  Used in 3D, where a fused pass A is
 // fp64-issue-bound.
-__global__ void __launch_bounds__(kEwThreads)
+__global__ void __launch_bounds__(kEwThreads, 4)  // 4 CTAs/SM: the grid is one full wave
     pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old,
              const double *p_old2, double *p_new, double *x, const lsg_pcg_scalars *scal) {
   const int rhs = blockIdx.y;
