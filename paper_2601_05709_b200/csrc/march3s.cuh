@@ -1,13 +1,14 @@
 // 3D z-marching kernel with an asynchronous shared-memory staging pipeline.
 //
 // Same decomposition as described in ops3d.cu (CTA = 8 warps = 8 node rows
-// incl. one halo row, 30 owned columns per warp, marching along z), but the
-// global loads of planes k+1 and k+2 are in flight as cp.async (LDGSTS)
-// copies into a 3-slot ring while plane k is computed: no registers are spent
-// on prefetching and no warp waits on a load it issued in the same step.  The
-// row above (y+1) is read from the staged plane and its operator input is
-// recomputed locally (3 FMAs per node), so the only cross-warp exchange left
-// is the y-contribution hand-off: two barriers per plane.
+// incl. one halo row, 30 owned columns per warp, marching along z).  The
+// global loads of planes k+1 and k+2 are in flight as 16-byte cp.async
+// (LDGSTS) copies into a 3-slot ring while plane k is computed, so no
+// registers are spent on prefetching and no warp waits on a load it issued in
+// the same step.  The row above (y+1) is read from the staged plane and its
+// operator input recomputed locally; the only cross-warp exchange is the
+// y-contribution hand-off, through a parity-double-buffered shared buffer:
+// one barrier per plane.  Plane states ping-pong between two register sets.
 #pragma once
 
 namespace lsg {
@@ -34,13 +35,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // verbatim with 16-byte copies into a 784-byte slot (the window starts 0 or 8
 // bytes into its first 16-byte chunk); lanes then read their node at a
 // 3-double stride (conflict-free for 64-bit shared loads).
-// Source arrays per row: APPLY/STATS: input; RESID: x, dinv; PCGA: r, p_old,
-// dinv, x; SHAPE: KB states.
+// Source arrays per row: APPLY/STATS: input; RESID: x, dinv; PCGQ: p;
+// SHAPE: KB states.
 constexpr int kRowSlot = 98;  // doubles: 49 chunks of 16 bytes
 
 template <class PH, int ACT>
 struct Stage {
-  static constexpr int NS = (ACT == PCGA) ? 4 : (ACT == RESID) ? 2 : PH::NIN / 3;  // PCGQ: p
+  static constexpr int NS = (ACT == RESID) ? 2 : PH::NIN / 3;  // APPLY/PCGQ/STATS: 1
   static constexpr int NOUT = PH::NOUT;
   static constexpr size_t doubles = (size_t)3 * (kWarps + 1) * NS * kRowSlot;
   static constexpr size_t words = (size_t)3 * (kWarps + 1) * 32;
@@ -97,41 +98,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   const int K1 = min(K0 + a.seg, nz + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * 3;
 
-  double beta = 0.0, alpha_prev = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA) {
-    lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0 || a.finish_only) {  // CTA-uniform
-      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      // converged after iteration L = iters - 1: alpha_L p_L and, for odd L,
-      // first alpha_{L-1} p_{L-1} are pending
-      const int L = (int)s.iters - 1;
-      const double al = s.alpha, al2 = s.reserved[2];
-      const bool two = s.reserved[1] > 1.5;
-      const double *pL = a.ring[L % 3] + voff, *pL1 = a.ring[(L + 2) % 3] + voff;
-      if (own) {
-        for (int kk = K0; kk < K1; ++kk) {
-          const int64_t node = ((int64_t)kk * nyp + jw) * nxp + i;
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            double xv = a.xs[voff + node * 3 + q];
-            if (two) xv = fma(al2, pL1[node * 3 + q], xv);
-            a.xs[voff + node * 3 + q] = fma(al, pL[node * 3 + q], xv);
-          }
-        }
-      }
-      double d1[1] = {0.0}, t1[1];
-      const int nblk = gridDim.x * gridDim.y * nzseg;
-      const int blk = ((int)zseg * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk, a.counters + rhs,
-                                         blk, nblk, scratch, t1))
-        if (threadIdx.x == 0) s.reserved[1] = 0.0;
-      return;
-    }
-    first = s.first != 0.0;
-    beta = s.beta;
-    alpha_prev = s.alpha;
-  } else if constexpr (ACT == RESID || ACT == PCGQ) {
+  if constexpr (ACT == RESID || ACT == PCGQ) {
     if (a.scal[rhs].done != 0.0) return;
   }
 
@@ -144,9 +111,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
 
   // source arrays staged per row
   const double *src[NS];
-  if constexpr (ACT == PCGA) {
-    src[0] = a.x + voff; src[1] = a.x2 + voff; src[2] = a.dinv; src[3] = a.xs + voff;
-  } else if constexpr (ACT == RESID) {
+  if constexpr (ACT == RESID) {
     src[0] = a.x + voff; src[1] = a.dinv;
   } else if constexpr (ACT == SHAPE) {
 #pragma unroll
@@ -222,25 +187,6 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
 #pragma unroll
         for (int q = 0; q < 3; ++q) dg[q] = V(1, q);
       }
-      if constexpr (ACT == PCGA) {
-        // p = D^-1 r + beta p_old (p_old is zeroed by pcg_start, beta = 0 first)
-        double po[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          dg[q] = V(2, q);
-          po[q] = V(1, q);
-          v[q] = fma(beta, po[q], v[q] * dg[q]);
-        }
-        if (write_own) {
-          const int64_t node = (int64_t)kk * plane + node_in_plane;
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            a.y2[voff + node * 3 + q] = v[q];
-            if (!first)  // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
-              a.xs[voff + node * 3 + q] = fma(alpha_prev, po[q], V(3, q));
-          }
-        }
-      }
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         raw[q] = v[q];
@@ -277,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
           part[1] += r * r;
           part[2] += r * (r * dg[q]);
         }
-      } else if constexpr (ACT == PCGA || ACT == PCGQ) {
+      } else if constexpr (ACT == PCGQ) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           a.y[voff + node * 3 + q] = yv[q];

@@ -434,26 +434,24 @@ struct Shape {
   }
 };
 
-// PCGQ: the apply half of a split pass A (q = A p, p.q; p formed by pcg_prep)
-enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4, PCGQ = 5 };
+// PCGQ: the stencil half of the split pass A (q = A p, p.q; p formed by pcg_prep)
+enum Act { APPLY = 0, RESID = 1, STATS = 3, SHAPE = 4, PCGQ = 5 };
 
 struct MArgs {
   const uint32_t *words;
   const double *x, *x2, *b;
   double *y, *y2;
   const double *dinv;
-  double *xs;  // PCGA (finish): the iterate x
-  const double *ring[3];  // PCGA finish: the three direction buffers
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
   double *out;
-  int seg, nzseg, nstrips, accumulate, finish_only;
+  int seg, nzseg, nstrips, accumulate;
 };
 
 template <int ACT>
 struct Traits {
-  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA || ACT == PCGQ) ? 1
+  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGQ) ? 1
                          : (ACT == STATS) ? 3 : (ACT == SHAPE) ? 2 : 0;
   static constexpr unsigned MAXMASK = (ACT == STATS) ? 4u : 0u;
 };
@@ -474,7 +472,7 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
     } else if (sqrt(tot[1]) < s.atol) {
       s.done = 1.0;
     }
-  } else if constexpr (ACT == PCGA || ACT == PCGQ) {
+  } else if constexpr (ACT == PCGQ) {
     lsg_pcg_scalars &s = a.scal[rhs];
     s.pq = tot[0];
     s.reserved[2] = s.alpha;  // alpha_{i-1}, still pending on odd iterations
@@ -1077,19 +1075,44 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   return LSG_OK;
 }
 
+// lsg_pcg_finish: apply the pending x updates of converged right-hand sides
+// (after iteration L = iters - 1: alpha_L p_L and, for odd L, first
+// alpha_{L-1} p_{L-1}), then clear the pending flags.
+__global__ void __launch_bounds__(kEwThreads)
+    pcg_finish_kernel(int64_t n, const double *r0, const double *r1, const double *r2, double *x,
+                      const lsg_pcg_scalars *scal) {
+  const int rhs = blockIdx.y;
+  const lsg_pcg_scalars &s = scal[rhs];
+  if (s.done == 0.0 || s.reserved[1] == 0.0) return;
+  const int L = (int)s.iters - 1;
+  const double *const ring[3] = {r0, r1, r2};
+  const size_t off = (size_t)rhs * (size_t)n;
+  const double *pL = ring[L % 3] + off, *pL1 = ring[(L + 2) % 3] + off;
+  const double al = s.alpha, al2 = s.reserved[2];
+  const bool two = s.reserved[1] > 1.5;
+  for (int64_t t = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * kEwThreads) {
+    double xv = x[off + t];
+    if (two) xv = fma(al2, pL1[t], xv);
+    x[off + t] = fma(al, pL[t], xv);
+  }
+}
+
+__global__ void clear_pending(int k, lsg_pcg_scalars *scal) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < k && scal[r].done != 0.0) scal[r].reserved[1] = 0.0;
+}
+
 int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
-  MArgs a = {};
-  a.x = ws.r;
-  a.ring[0] = ws.p;
-  a.ring[1] = ws.p_alt;
-  a.ring[2] = ws.p_ring;
-  a.dinv = ws.dinv;
-  a.xs = ws.x;
-  a.scal = ws.scal;
-  a.partials = ws.partials;
-  a.counters = ws.counters;
-  a.finish_only = 1;
-  return dispatch<PCGA>(op, a, ws.k, st);
+  const int64_t n = 3 * nodes_of(geo_of(op.grid));
+  int64_t nb = ceil_div(n, kEwThreads);
+  if (nb > 4 * kSMs) nb = 4 * kSMs;
+  pcg_finish_kernel<<<dim3((unsigned)nb, (unsigned)ws.k), kEwThreads, 0, st>>>(
+      n, ws.p, ws.p_alt, ws.p_ring, ws.x, ws.scal);
+  int rc = check_launch("pcg_finish3d");
+  if (rc) return rc;
+  clear_pending<<<(unsigned)ceil_div(ws.k, 64), 64, 0, st>>>(ws.k, ws.scal);
+  return check_launch("clear_pending3d");
 }
 
 template <int KB>
