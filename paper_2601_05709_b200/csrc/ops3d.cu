@@ -946,8 +946,14 @@ static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int 
     smax = e ? atoi(e) : 32;
     if (smax < 6) smax = 6;
   }
+  static int smin = -1;  // LSG_M3_SEGMIN: floor on planes per segment (experiments)
+  if (smin < 0) {
+    const char *e = getenv("LSG_M3_SEGMIN");
+    smin = e ? atoi(e) : 6;
+    if (smin < 2) smin = 2;
+  }
   if (s > smax) s = smax;
-  if (s < 6) s = 6;
+  if (s < smin) s = smin;
   while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
   seg = (int)s;
   nzseg = (int)ceil_div(g.nz + 1, s);
