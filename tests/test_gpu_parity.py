@@ -147,6 +147,18 @@ class TestSolve:
         np.testing.assert_array_equal(host(x1), host(x2))
 
 
+    def test_iteration_cap_raises_solver_error_with_true_residual(self, setup32):
+        """scipy cg semantics (fem.py:309-315): maxiter exhausted -> SolverError(residual)
+        carrying the true residual of the failing right-hand side."""
+        mesh, space, phi, model, _ = setup32
+        op = model.operator(phi)
+        b = model.load_vectors[:1]
+        with pytest.raises(lsg.SolverError) as err:
+            solve_batched(op, b, rtol=1e-14, atol=0.0, maxiter=5)
+        assert err.value.residual > 0.0 and np.isfinite(err.value.residual)
+        assert "5 iterations" in str(err.value)
+
+
 class TestDerivativeAndVelocity:
     def test_s1_tensor(self, golden, setup32):
         mesh, space, phi, model, _ = setup32

@@ -190,6 +190,25 @@ def test_batched_zero_and_nonzero(both):
     assert float(x[0].abs().max()) == 0.0 and int(it[0]) == 0 and int(it[1]) > 0
 
 
+def test_iteration_cap_and_odd_batch(both):
+    """3D: k = 3 right-hand sides of different scale against the oracle's scipy cg,
+    and the iteration cap raising SolverError(residual)."""
+    mesh, grid, space, ospace, phi = both
+    om, gm, lp, bil = _model_pair(both)
+    op = gm.operator(lp)
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal((3, space.dof_count)) * np.array([[1.0], [1e-3], [1e2]])
+    b[:, gm.bc.dofs] = 0.0
+    x, it = solve_batched(op, torch.as_tensor(b, device="cuda"), rtol=1e-12)
+    A, _ = ofem.dirichlet_eliminate(om.matrix(phi), np.zeros(space.dof_count), om.clamp)
+    for r in range(3):
+        xr, _ = ofem.jacobi_pcg(A, b[r], rtol=1e-12)
+        assert rel_l2(host(x[r]), xr) <= 1e-8
+    with pytest.raises(lsg.SolverError) as err:
+        solve_batched(op, torch.as_tensor(b[:1], device="cuda"), rtol=1e-14, atol=0.0, maxiter=4)
+    assert err.value.residual > 0.0
+
+
 def test_cfg3_coarse_history_matches_oracle():
     """cfg3 geometry at 12x6x6 (scale 8), 6 iterations with one reinit."""
     from oracle import cases as ocases, driver as odriver
