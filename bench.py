@@ -34,6 +34,11 @@ FALLBACK_HBM = 6650.0
 # (profiles/r01_bench_notes.md); used to extrapolate the bounded CPU sample to
 # a whole iteration.  Same algorithm and stopping rule on both sides.
 CFG2_RHS_ITERS_PER_OUTER = 127687.0
+# PCG right-hand-side iterations per outer iteration measured on the B200 runs
+# (tools/loop_profile.py; cfg4 = its one solve to 1e-8), used to extrapolate the
+# bounded CPU samples of the reference arm
+RHS_ITERS_PER_OUTER = {"cfg1": 2132.0, "cfg2": CFG2_RHS_ITERS_PER_OUTER, "cfg3": 2200.0,
+                       "cfg4": 197320.0, "cfg5": 17079.0}
 
 
 def parse():
@@ -380,7 +385,7 @@ def reference_arm(args, world, rank, local):
     vals = []
     for i in range(args.warmup + args.steps):
         s = cpu_sample(c, cg_iters_per_load=10, threads=threads)
-        v, t_outer = cpu_iters_per_sec(s, CFG2_RHS_ITERS_PER_OUTER)
+        v, t_outer = cpu_iters_per_sec(s, RHS_ITERS_PER_OUTER[args.config])
         if i >= args.warmup:
             vals.append(t_outer)
     t_outer = statistics.median(vals)
@@ -394,7 +399,7 @@ def reference_arm(args, world, rank, local):
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": threads, "kind": "port",
                          "sample": "per step: oracle assembly + 10 scipy-cg PCG iterations per load "
                                    f"({threads} threads, reference task_parallel mode) + S1/RHS + "
-                                   f"transport, extrapolated with {CFG2_RHS_ITERS_PER_OUTER:.0f} "
+                                   f"transport, extrapolated with {RHS_ITERS_PER_OUTER[args.config]:.0f} "
                                    "PCG rhs-iterations per outer iteration"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
