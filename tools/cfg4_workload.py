@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""The BASELINE cfg4 operator stress test, end to end on one B200 (CUDA events).
+
+    python tools/cfg4_workload.py [--scale 1]
+
+4096x2048 P1 mesh (16.8M dofs), Gaussian-random-field level set, bottom clamp,
+body force (0,-1): setup (mesh, level set, material words, loads, inverse
+diagonal), 200 stiffness applies, one Jacobi-PCG solve to relative residual
+1e-8 from zero, one S0/S1 evaluation (J, C, contracted derivative vectors)
+and one H1 descent solve.  Prints one JSON line with the time of each phase.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2601_05709_b200 import FemField, VelocitySolver, combine_derivatives, configs  # noqa: E402
+from paper_2601_05709_b200.fem import solve_batched  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=int, default=1)
+    args = ap.parse_args()
+    stream = torch.cuda.current_stream()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    e0 = ev()
+    c = configs.case("cfg4", scale=args.scale)
+    mesh, model, phi, _ = configs.build(c)
+    op = model.operator(phi)
+    op.inverse_diagonal()
+    e1 = ev()
+    u = torch.randn((1, model.space.dof_count), dtype=torch.float64, device="cuda")
+    y = None
+    for _ in range(200):
+        y = op.apply(u)
+    e2 = ev()
+    x, it = solve_batched(op, model.load_vectors, rtol=1e-8)
+    e3 = ev()
+    state = FemField(model.space, x[0])
+    J = model.cost(phi, [state])
+    C = model.constraint(phi, [state])
+    cost_pair, cons = model.derivative(phi, [state], None)
+    e4 = ev()
+    solver = VelocitySolver(model.bilinear_form(), model.space)
+    res = solver.solve(combine_derivatives(cost_pair, cons, np.array([0.1])))
+    e5 = ev()
+    torch.cuda.synchronize()
+    ms = lambda a, b: a.elapsed_time(b)
+    out = {"config": f"cfg4 scale {args.scale}", "n": list(mesh.n), "dofs": model.space.dof_count,
+           "setup_ms": ms(e0, e1), "apply_200_ms": ms(e1, e2), "apply_us": 1e3 * ms(e1, e2) / 200,
+           "pcg_ms": ms(e2, e3), "pcg_iterations": int(it[0]), "pcg_us_per_iteration": 1e3 * ms(e2, e3) / max(int(it[0]), 1),
+           "s0s1_ms": ms(e3, e4), "h1_ms": ms(e4, e5), "h1_iterations": solver.last_iterations,
+           "total_ms": ms(e0, e5), "J": J, "C": float(C[0]), "form_value": res.form_value,
+           "checksum_y": float(y.sum())}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
