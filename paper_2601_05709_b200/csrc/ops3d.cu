@@ -33,7 +33,10 @@ namespace lsg {
 namespace d3 {
 
 constexpr int kStrip = 30;
-constexpr int kWarps = 8;
+#ifndef LSG_M3_WARPS
+#define LSG_M3_WARPS 8
+#endif
+constexpr int kWarps = LSG_M3_WARPS;  // node rows per CTA (one of them halo)
 constexpr int kThreads = kWarps * 32;
 constexpr int kSMs = 148;
 constexpr int kMaxPartials = 4096;
