@@ -187,3 +187,21 @@ def test_toml_inverse_and_heat_models_run():
         model, phi = build_model(cfg, mesh), build_initial(cfg, mesh)
         _, hist = lsg.run(model, phi, cfg.params, timing=False)
         assert len(hist) == 3 and all(np.isfinite(r.cost) for r in hist)
+
+
+def test_cfg1_full_size_history_matches_oracle():
+    """BASELINE cfg1 at its own size (160x80, all 50 iterations, reinit every 5): J, C,
+    Lagrangian, B(theta, theta) within 1e-4 of the oracle's run at every iteration and
+    identical discrete counters (tests/golden/make_golden_cfg1_full.py)."""
+    import os
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_cfg1_full.npz"))
+    mesh, model, phi, params = configs.build(configs.case("cfg1"))
+    _, hist = lsg.run(model, phi, params, timing=False)
+    assert len(hist) == len(gold["cost"]) == 50
+    np.testing.assert_allclose([r.cost for r in hist], gold["cost"], rtol=1e-4)
+    np.testing.assert_allclose([r.constraint[0] for r in hist], gold["constraint"], rtol=1e-4)
+    np.testing.assert_allclose([r.lagrangian for r in hist], gold["lagrangian"], rtol=1e-4)
+    np.testing.assert_allclose([r.form_value for r in hist], gold["form_value"], rtol=1e-4)
+    np.testing.assert_array_equal([r.steps for r in hist], gold["steps"])
+    np.testing.assert_array_equal([r.transport_substeps for r in hist], gold["nsub_transport"])
+    np.testing.assert_array_equal([r.reinit_substeps for r in hist], gold["nsub_reinit"])
