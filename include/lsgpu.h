@@ -37,6 +37,7 @@ extern "C" {
 #define LSG_OK 0
 #define LSG_ERR_ARG -1
 #define LSG_ERR_CUDA -2
+#define LSG_ERR_NOCONV -3 /* an iterative solve missed its tolerance (SolverError) */
 
 /* Structured box mesh [lo, hi] with n[a] cells per axis; dim = 2 (right
  * triangles split along the lower-left/upper-right diagonal, mesh.py:140-150)
@@ -303,10 +304,13 @@ int lsg_reinit(const lsg_grid *g, const double *phi_in, double dt, int32_t nsub,
  * rhs = m_hat cur + dt (load + diffusion), PG_REINIT operator (aux[0..2]). */
 int lsg_pg_reinit_rhs(const lsg_op *op, double *rhs, void *stream);
 
-/* Right-Jacobi-preconditioned BiCGStab for a PG operator: A x = b to
- * ||r|| <= rtol ||b|| (x holds the initial guess).  Unlike the other entry
- * points it synchronises `stream` once per iteration to test convergence.
- * work: lsg_bicgstab_work_doubles(g) doubles of device memory. */
+/* Solve A x = b for a PG operator to ||r|| <= rtol ||b|| (x holds the initial
+ * guess) -- the reference factorises these matrices with splu
+ * (levelset.py:165,204).  Right-Jacobi BiCGStab first; if it stagnates or
+ * breaks down, restarted GMRES(48) with CGS2 from the same initial guess;
+ * LSG_ERR_NOCONV if neither converges within maxit iterations.  Unlike the
+ * other entry points it synchronises `stream` per iteration to test
+ * convergence.  work: lsg_bicgstab_work_doubles(g) doubles of device memory. */
 int64_t lsg_bicgstab_work_doubles(const lsg_grid *g);
 int lsg_bicgstab(const lsg_op *op, const double *b, double *x, double *work, double rtol,
                  int32_t maxit, int32_t *iters, double *resid, void *stream);

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("LSG_LIB_PATH") or os.path.join(os.path.dirname(os.pat
 LSG_OK = 0
 LSG_ERR_ARG = -1
 LSG_ERR_CUDA = -2
+LSG_ERR_NOCONV = -3
 LSG_OP_ELASTICITY = 1
 LSG_OP_H1 = 2
 LSG_OP_PG_TRANSPORT = 3
@@ -127,6 +128,8 @@ def call(name, *args):
         msg = lib.lsg_last_error().decode(errors="replace")
         if rc == LSG_ERR_ARG:
             raise ConfigError(f"{name}: {msg}")
+        if rc == LSG_ERR_NOCONV:
+            raise SolverError(f"{name}: {msg}")
         raise RuntimeError(f"{name}: {msg}")
     return rc
 

@@ -169,7 +169,10 @@ int64_t lsg_bicgstab_work_doubles(const lsg_grid *g) {
   if (check_grid(g)) return -1;
   int64_t nn = 1;
   for (int a = 0; a < g->dim; ++a) nn *= (int64_t)g->n[a] + 1;
-  return 9 * nn + 16 + 2 * 296 + 8;
+  // saved initial guess + max(BiCGStab workspace, GMRES(m) workspace)
+  const int64_t bicg = 9 * nn + 16 + 2 * 296 + 8;
+  const int64_t gm = pg::gmres_work_doubles(nn);
+  return nn + (bicg > gm ? bicg : gm);
 }
 
 int lsg_bicgstab(const lsg_op *op, const double *b, double *x, double *work, double rtol,

@@ -77,6 +77,7 @@ namespace pg {  // the reference's own level-set scheme, 2D (pg2d.cu)
 int apply(const lsg_op &op, const double *x, double *y, cudaStream_t st);
 int diag(const lsg_op &op, double *d, cudaStream_t st);
 int reinit_rhs(const lsg_op &op, double *rhs, cudaStream_t st);
+int64_t gmres_work_doubles(int64_t n);
 int bicgstab(const lsg_op &op, const double *b, double *x, double *work, double rtol, int maxit,
              int *iters, double *resid, cudaStream_t st);
 }  // namespace pg

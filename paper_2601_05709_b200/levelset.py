@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigError
+from .errors import ConfigError, SolverError
 from .fem import FemField, FunctionSpace, to_device
 from .mesh import mesh_diameter
 
@@ -153,12 +153,20 @@ def _check_velocity_field(phi, theta):
 PG_RTOL = 1e-14  # BiCGStab tolerance of the reference scheme's step solves (reference: SuperLU)
 
 
+BICG_LOG = None  # set to a list to record (iterations, relative residual) per solve
+
+
 def _bicgstab(op, b, x, mesh):
     work = _SCRATCH.get(mesh, "bicg_work", int(_lib.load().lsg_bicgstab_work_doubles(mesh.grid)))
     iters = ctypes.c_int32(0)
     resid = ctypes.c_double(0.0)
-    _lib.call("lsg_bicgstab", op, _lib.ptr(b), _lib.ptr(x), _lib.ptr(work), PG_RTOL, 2000,
-              ctypes.byref(iters), ctypes.byref(resid), _lib.stream())
+    try:
+        _lib.call("lsg_bicgstab", op, _lib.ptr(b), _lib.ptr(x), _lib.ptr(work), PG_RTOL, 4000,
+                  ctypes.byref(iters), ctypes.byref(resid), _lib.stream())
+    except SolverError as exc:
+        raise SolverError(str(exc), residual=float(resid.value)) from None
+    if BICG_LOG is not None:
+        BICG_LOG.append((int(iters.value), float(resid.value)))
     return int(iters.value)
 
 
