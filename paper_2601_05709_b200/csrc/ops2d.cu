@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)
       s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending (next pass A / finish)
       if (sqrt(tot[1]) < s.atol) {
         s.done = 1.0;
-      } else if (s.iters >= s.maxiter) {
+      } else if (s.iters >= s.maxiter || !isfinite(tot[1]) || !isfinite(tot[0])) {
         s.done = 2.0;  // iteration cap exhausted: SolverError on the host
       } else {
         s.beta = tot[0] / s.rho;
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kThreads)
           s_iters[r] += 1.0;
           int done = 0;
           if (sqrt(rr) < s_atol[r]) done = 1;
-          else if (s_iters[r] >= s_maxit[r]) done = 2;
+          else if (s_iters[r] >= s_maxit[r] || !isfinite(rr) || !isfinite(rz)) done = 2;
           else {
             s_beta[r] = rz / s_rho[r];
             s_rho[r] = rz;

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kEwThreads)
       s.rr = tot[1];
       s.reserved[1] = (((int)s.iters - 1) & 1) ? 2.0 : 1.0;  // pending x updates (as 2D)
       if (sqrt(tot[1]) < s.atol) s.done = 1.0;
-      else if (s.iters >= s.maxiter) s.done = 2.0;
+      else if (s.iters >= s.maxiter || !isfinite(tot[1]) || !isfinite(tot[0])) s.done = 2.0;
       else {
         s.beta = tot[0] / s.rho;
         s.rho = tot[0];

@@ -158,6 +158,21 @@ class TestSolve:
         assert err.value.residual > 0.0 and np.isfinite(err.value.residual)
         assert "5 iterations" in str(err.value)
 
+    def test_non_finite_fails_fast(self, setup32):
+        """A NaN iterate stops its right-hand side at once (SolverError) instead of
+        running to the 10n cap; the other right-hand side of the batch still converges."""
+        mesh, space, phi, model, _ = setup32
+        op = model.operator(phi)
+        b = torch.stack([model.load_vectors[0], model.load_vectors[0]])
+        x0 = torch.zeros_like(b)
+        x0[0, 7] = float("nan")
+        with pytest.raises(lsg.SolverError) as err:
+            solve_batched(op, b, x0)
+        n_it = int(str(err.value).split("after ")[1].split(" ")[0])
+        assert n_it <= 2
+        x, it = solve_batched(op, b[1:])
+        assert torch.isfinite(x).all() and int(it[0]) > 10
+
 
 class TestDerivativeAndVelocity:
     def test_s1_tensor(self, golden, setup32):

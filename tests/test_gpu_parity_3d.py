@@ -207,6 +207,11 @@ def test_iteration_cap_and_odd_batch(both):
     with pytest.raises(lsg.SolverError) as err:
         solve_batched(op, torch.as_tensor(b[:1], device="cuda"), rtol=1e-14, atol=0.0, maxiter=4)
     assert err.value.residual > 0.0
+    x0 = torch.zeros((1, space.dof_count), dtype=torch.float64, device="cuda")
+    x0[0, 5] = float("inf")
+    with pytest.raises(lsg.SolverError) as err:  # non-finite: stops at once, not at 10n
+        solve_batched(op, torch.as_tensor(b[:1], device="cuda"), x0)
+    assert int(str(err.value).split("after ")[1].split(" ")[0]) <= 3
 
 
 def test_cfg3_coarse_history_matches_oracle():
