@@ -289,7 +289,10 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 // One marching task (strip group bx, row segment by, right-hand side rhs):
 // the body shared by the per-launch kernel below and the persistent PCG.
 // Adds this thread's reduction terms to part[].
-template <class PH, int ACT, class W>
+// COH: the inputs were written earlier in the same launch (the persistent PCG
+// kernel, across grid barriers), so they are read with coherent loads instead of
+// the read-only (non-coherent) path.
+template <class PH, int ACT, class W, bool COH = false>
 __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MArgs &a, int bx,
                                            int by, int rhs, bool first, double beta,
                                            double alpha_prev,
@@ -336,11 +339,14 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
 #pragma unroll
       for (int k = 0; k < NF; ++k) ldg_node<NC>(xin + (size_t)k * nn * NC, off, f.v[k]);
     } else {
-      ldg_node<NC>(xin, off, f.v[0]);
+      if constexpr (COH) ld_node<NC>(xin, off, f.v[0]);
+      else ldg_node<NC>(xin, off, f.v[0]);
       if constexpr (ACT == PCGA) {
         if (first) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) f.v[1][c] = 0.0;
+        } else if constexpr (COH) {
+          ld_node<NC>(xin2, off, f.v[1]);
         } else {
           ldg_node<NC>(xin2, off, f.v[1]);
         }

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double scratch[2 * KMAX * kWarps];
   __shared__ double s_beta[KMAX], s_alpha[KMAX], s_rho[KMAX], s_atol[KMAX], s_iters[KMAX];
   __shared__ double s_maxit[KMAX], s_pa[KMAX];
-  __shared__ int s_first[KMAX], s_done[KMAX], s_all;
+  __shared__ int s_first[KMAX], s_done[KMAX], s_newly[KMAX], s_all;
   const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
   const int ncta = gridDim.x, cta = blockIdx.x;
   double *pa = pbuf, *pb = pbuf + (size_t)ncta * KMAX;  // [ncta][KMAX], [ncta][2 KMAX]
@@ -517,13 +517,16 @@ __global__ void __launch_bounds__(kThreads)
     aa.x2 = parity ? p_odd : p_even;  // p_old
     aa.y2 = parity ? p_even : p_odd;  // p_new
     // pass A: p = M^-1 r + beta p_old, q = A p, p.q partials, pending x update
-    if (threadIdx.x < KMAX) s_pa[threadIdx.x] = 0.0;
+    if (threadIdx.x < KMAX) {
+      s_pa[threadIdx.x] = 0.0;
+      s_newly[threadIdx.x] = 0;
+    }
     __syncthreads();
     for (int t = cta; t < ntask; t += ncta) {
       const int rhs = t / (tx * ty), rem = t - rhs * (tx * ty);
       if (s_done[rhs]) continue;
       double part[1] = {0.0};
-      march_core<PH, PCGA, uint8_t>(ph, g, aa, rem % tx, rem / tx, rhs, s_first[rhs] != 0,
+      march_core<PH, PCGA, uint8_t, true>(ph, g, aa, rem % tx, rem / tx, rhs, s_first[rhs] != 0,
                                    s_beta[rhs], s_alpha[rhs], part);
       block_reduce<1, 0u>(part, scratch);
       if (threadIdx.x == 0) s_pa[rhs] += part[0];
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(kThreads)
       for (int64_t node = (int64_t)cta * kThreads + threadIdx.x; node < nn;
            node += (int64_t)ncta * kThreads) {
         double Q[NC], R[NC], D[NC];
-        ldg_node<NC>(qv, node, Q);
+        ld_node<NC>(qv, node, Q);  // written by pass A of this launch: coherent load
         ldg_node<NC>(a.dinv, node, D);
         ld_node<NC>(rv, node, R);
 #pragma unroll
@@ -600,12 +603,15 @@ __global__ void __launch_bounds__(kThreads)
             s_first[r] = 0;
           }
           s_done[r] = done != 0;
+          s_newly[r] = done != 0;
           if (cta == 0) {
             lsg_pcg_scalars &sc = a.scal[r];
             sc.iters = s_iters[r];
             sc.rz_new = rz;
             sc.rr = rr;
-            sc.reserved[1] = 1.0;  // x += alpha p of this iteration is pending
+            // x += alpha p of this iteration: folded into the next pass A while the
+            // RHS runs, applied just below (in this launch) once it has stopped
+            sc.reserved[1] = done ? 0.0 : 1.0;
             sc.alpha = s_alpha[r];
             if (done) sc.done = (double)done;
             else {
@@ -617,6 +623,25 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
       __syncthreads();
+    }
+    // right-hand sides that stopped in this iteration: their last x += alpha p now,
+    // while p_new still holds their last direction (later iterations flip the
+    // buffers; no other pass touches their x again)
+#pragma unroll
+    for (int r = 0; r < KMAX; ++r) {
+      if (!s_newly[r]) continue;
+      const double alpha = s_alpha[r];
+      double *xv = a.xs + (size_t)r * nn * NC;
+      const double *pv = aa.y2 + (size_t)r * nn * NC;
+      for (int64_t node = (int64_t)cta * kThreads + threadIdx.x; node < nn;
+           node += (int64_t)ncta * kThreads) {
+        double X[NC], P[NC];
+        ld_node<NC>(xv, node, X);
+        ld_node<NC>(pv, node, P);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) X[c] = fma(alpha, P[c], X[c]);
+        st_node<NC>(xv, node, X);
+      }
     }
   }
 }

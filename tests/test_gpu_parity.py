@@ -86,9 +86,7 @@ class TestOperator:
         got = host(op.apply(u))
         for g, ref in zip(got, golden["apply_Ku"]):
             assert rel_l2(g, ref) <= 1e-10
-        for g, ref in zip(got, golden["apply_Ku"]):  # batch == single
-            pass
-        single = host(op.apply(u[1]))
+        single = host(op.apply(u[1]))  # batch == single, bitwise
         np.testing.assert_array_equal(single, got[1])
 
     def test_apply_eliminated_and_diag(self, golden, setup32):
