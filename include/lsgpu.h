@@ -107,17 +107,20 @@ typedef struct {
 } lsg_pcg_scalars;
 
 /* PCG workspace; every pointer is device memory owned by the caller.
- *   x, b, r, p, q, p_alt : k * n doubles each (n = dim * num_nodes)
+ *   x, b, r, p, q, p_alt : k * n doubles each (n = dim * num_nodes);
+ *   r_alt, q_alt  : k * n doubles each (2D), p_ring: k * n doubles (3D)
  *   scal          : k lsg_pcg_scalars
- *   partials      : k * lsg_partials_per_rhs() * 4 doubles
+ *   partials      : k * lsg_partials_per_rhs() * 8 doubles
  *   counters      : k uint32, zero-initialised once by the caller
  *   dinv          : n doubles, lsg_inv_diag of the operator (shared by all k)
- * The search direction is double-buffered (p / p_alt): the fused pass that
- * forms p = z + beta p_old also applies the operator to it, and neighbouring
- * CTAs read p_old in their halo, so p cannot be updated in place.  `parity`
- * (which buffer is current) is owned by the library: lsg_pcg_start resets it,
- * lsg_pcg_iterate flips it once per iteration; the current direction after a
- * call is (parity ? p_alt : p). */
+ * 2D runs one fused pass per iteration: it forms r_i = r_{i-1} - alpha q_{i-1},
+ * z = M^-1 r_i, p_i = z + beta p_{i-1}, x += alpha p_{i-1} and q_i = A p_i with
+ * neighbouring CTAs recomputing r_i and p_i in their halo, so r, p and q are
+ * double-buffered (r/r_alt, p/p_alt, q/q_alt).  3D runs an elementwise pass
+ * that forms p, the stencil pass, and an update pass, with three direction
+ * buffers (p, p_alt, p_ring).  `parity` (which buffers are current) is owned
+ * by the library: lsg_pcg_start resets it, lsg_pcg_iterate advances it once
+ * per iteration. */
 typedef struct {
   int32_t k;
   int32_t parity;
@@ -133,6 +136,8 @@ typedef struct {
   const double *dinv; /* n doubles: inverse Jacobi diagonal from lsg_inv_diag */
   double *p_ring;     /* 3D: third direction buffer (k x n); x is updated every
                          second iteration with two directions at once */
+  double *r_alt;      /* 2D: second residual buffer (k x n) */
+  double *q_alt;      /* 2D: second A p buffer (k x n) */
 } lsg_pcg_ws;
 
 int32_t lsg_abi_version(void);

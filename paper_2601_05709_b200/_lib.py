@@ -51,7 +51,8 @@ class PcgWs(ctypes.Structure):
                 ("x", ctypes.c_void_p), ("b", ctypes.c_void_p), ("r", ctypes.c_void_p),
                 ("p", ctypes.c_void_p), ("q", ctypes.c_void_p), ("scal", ctypes.c_void_p),
                 ("partials", ctypes.c_void_p), ("counters", ctypes.c_void_p),
-                ("p_alt", ctypes.c_void_p), ("dinv", ctypes.c_void_p), ("p_ring", ctypes.c_void_p)]
+                ("p_alt", ctypes.c_void_p), ("dinv", ctypes.c_void_p), ("p_ring", ctypes.c_void_p),
+                ("r_alt", ctypes.c_void_p), ("q_alt", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

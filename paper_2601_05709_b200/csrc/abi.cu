@@ -82,7 +82,7 @@ using namespace lsg;
 
 extern "C" {
 
-int32_t lsg_abi_version(void) { return 2; }
+int32_t lsg_abi_version(void) { return 3; }
 int64_t lsg_launch_count(void) { return (int64_t)g_launches.load(); }
 const char *lsg_last_error(void) { return g_err; }
 

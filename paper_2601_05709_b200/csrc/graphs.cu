@@ -1,6 +1,6 @@
 // CUDA-graph replay of PCG iteration chunks.
 //
-// One lsg_pcg_iterate(niter) call is 2*niter kernel launches whose arguments
+// One lsg_pcg_iterate(niter) call is niter (2D) or 3*niter (3D) kernel launches whose arguments
 // depend only on (operator, workspace, parity, niter).  The first call with a
 // given argument set is captured on a private stream (capture records, it does
 // not execute) and instantiated; every call launches the instantiated graph on

@@ -7,19 +7,24 @@
 namespace lsg {
 namespace d2 {
 
-enum Act { APPLY = 0, RESID = 1, PCGA = 2, STATS = 3, SHAPE = 4 };
+enum Act { APPLY = 0, RESID = 1, PCG = 2, STATS = 3, SHAPE = 4 };
+
+#ifndef LSG_M2_PCG_MINB
+#define LSG_M2_PCG_MINB 1  // resident CTAs per SM the PCG pass is register-capped for
+#endif
 
 // Arguments shared by every marching launch (unused fields stay null).
 struct MArgs {
   const void *words;
-  const double *x;     // APPLY/RESID/STATS: input field ; PCGA: r ; SHAPE: u (KB fields)
-  const double *x2;    // PCGA: p_old ; STATS: vec
+  const double *x;     // APPLY/RESID/STATS: input field ; PCG: r_{i-1} ; SHAPE: u (KB fields)
+  const double *x2;    // PCG: p_{i-1} ; STATS: vec
+  const double *x3;    // PCG: q_{i-1}
   const double *b;     // RESID: b
-  double *y;           // APPLY: y ; RESID: r ; PCGA: q ; SHAPE: vec_cost
-  double *y2;          // PCGA: p (written) ; SHAPE: vec_vol
-  const double *dinv;  // RESID / PCGA: inverse Jacobi diagonal (1 on Dirichlet dofs)
-  double *xs;          // PCGA: the iterate x (x += alpha_prev p_old is done here)
-  int finish_only;     // PCGA: only apply pending x updates of converged rhs
+  double *y;           // APPLY: y ; RESID: r ; PCG: q_i ; SHAPE: vec_cost
+  double *y2;          // PCG: p_i ; SHAPE: vec_vol
+  double *y3;          // PCG: r_i
+  const double *dinv;  // RESID / PCG: inverse Jacobi diagonal (1 on Dirichlet dofs)
+  double *xs;          // PCG: the iterate x (x += alpha_{i-1} p_{i-1} is done here)
   lsg_pcg_scalars *scal;
   double *partials;
   uint32_t *counters;
@@ -218,7 +223,7 @@ struct HeatShape {
 
 template <class PH, int ACT>
 struct Traits {
-  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCGA) ? 1 : (ACT == STATS) ? 3
+  static constexpr int NP = (ACT == RESID) ? 3 : (ACT == PCG) ? 5 : (ACT == STATS) ? 3
                                                                      : (ACT == SHAPE) ? 2 : 0;
   static constexpr unsigned MAXMASK = (ACT == STATS) ? 4u : 0u;
 };
@@ -242,6 +247,44 @@ __device__ __forceinline__ void node_diag<H1>(const H1 &ph, uint32_t w00, uint32
   ph.diag(w00, wm0, w0m, wmm, i, j, d);
 }
 
+// End of single-pass PCG iteration i for one right-hand side, from the five
+// sums of the pass: tot = {p.q, z.q, q.M^-1 q, r.z, r.r} of p_i, q_i = A p_i,
+// z_i = M^-1 r_i and the explicit residual r_i = r_{i-1} - alpha_{i-1} q_{i-1}.
+// scipy cg's stopping rule on ||r_i|| (x already holds x_i: the pass folded
+// x += alpha_{i-1} p_{i-1} in), else alpha_i = r_i.z_i / p_i.q_i and
+//   rz_{i+1} = rz_i - 2 alpha_i z_i.q_i + alpha_i^2 q_i.M^-1 q_i,
+// the exact expansion of (r_i - alpha q_i).M^-1(r_i - alpha q_i), so that
+// beta_{i+1} = rz_{i+1} / rz_i is known before the pass that forms r_{i+1}
+// (one reduction per iteration: D'Azevedo, Eijkhout & Romine's reduced-
+// synchronisation CG).  rz itself is recomputed exactly every pass.
+__device__ __forceinline__ void pcg_decide(lsg_pcg_scalars &s, const double *tot) {
+  const double pq = tot[0], zq = tot[1], qdq = tot[2], rz = tot[3], rr = tot[4];
+  s.rr = rr;
+  s.pq = pq;
+  if (s.first == 0.0) {
+    s.iters += 1.0;
+    if (sqrt(rr) < s.atol) {
+      s.done = 1.0;
+      return;
+    }
+    if (s.iters >= s.maxiter || !isfinite(rr) || !isfinite(rz)) {
+      s.done = 2.0;
+      return;
+    }
+  }
+  const double alpha = rz / pq;
+  const double rz_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, zq, rz));
+  if (!isfinite(alpha) || !isfinite(rz_next)) {  // breakdown: report, do not spin
+    s.done = 2.0;
+    return;
+  }
+  s.rho = rz;
+  s.alpha = alpha;
+  s.beta = rz_next / rz;
+  s.rz_new = rz_next;
+  s.first = 0.0;
+}
+
 template <int ACT>
 __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *tot) {
   if constexpr (ACT == RESID) {
@@ -259,10 +302,8 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
     } else if (sqrt(tot[1]) < s.atol) {
       s.done = 1.0;
     }
-  } else if constexpr (ACT == PCGA) {
-    lsg_pcg_scalars &s = a.scal[rhs];
-    s.pq = tot[0];
-    s.alpha = s.rho / tot[0];
+  } else if constexpr (ACT == PCG) {
+    pcg_decide(a.scal[rhs], tot);
   } else if constexpr (ACT == STATS) {
     a.out[0] = tot[0];
     a.out[1] = tot[1];
@@ -289,18 +330,15 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 // One marching task (strip group bx, row segment by, right-hand side rhs):
 // the body shared by the per-launch kernel below and the persistent PCG.
 // Adds this thread's reduction terms to part[].
-// COH: the inputs were written earlier in the same launch (the persistent PCG
-// kernel, across grid barriers), so they are read with coherent loads instead of
-// the read-only (non-coherent) path.
-template <class PH, int ACT, class W, bool COH = false>
+template <class PH, int ACT, class W>
 __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MArgs &a, int bx,
-                                           int by, int rhs, bool first, double beta,
-                                           double alpha_prev,
+                                           int by, int rhs,
                                            double (&part)[Traits<PH, ACT>::NP > 0 ? Traits<PH, ACT>::NP : 1]) {
   constexpr int NC = PH::NC;  // components per node of each input field
   constexpr int NIN = PH::NIN, NOUT = PH::NOUT;
   constexpr int NF = (ACT == SHAPE) ? NIN / NC : 1;  // fields read per node (SHAPE: states)
-  constexpr bool HAS_DINV = (ACT == RESID || ACT == PCGA);
+  constexpr bool HAS_DINV = (ACT == RESID);
+  static_assert(ACT != PCG, "the PCG pass is march_pcg");
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int strip = bx * kWarps + warp;
@@ -317,14 +355,12 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
   const int J1 = min(J0 + a.seg, ny + 1);
   const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
   const double *xin = a.x + voff + (size_t)ic * NC;
-  const double *xin2 = (ACT == PCGA ? a.x2 + voff : a.x) + (size_t)ic * NC;
   const double *dvin = (HAS_DINV ? a.dinv : a.x) + (size_t)ic * NC;
   const W *win = words + ic;
 
   struct Raw {
-    double v[NF + (ACT == PCGA ? 1 : 0)][NC];
+    double v[NF][NC];
     double dv[NC];
-    double xv[NC];  // PCGA: x of an owned node (updated with the previous alpha)
     uint32_t wc;
   };
   struct Row {
@@ -339,19 +375,7 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
 #pragma unroll
       for (int k = 0; k < NF; ++k) ldg_node<NC>(xin + (size_t)k * nn * NC, off, f.v[k]);
     } else {
-      if constexpr (COH) ld_node<NC>(xin, off, f.v[0]);
-      else ldg_node<NC>(xin, off, f.v[0]);
-      if constexpr (ACT == PCGA) {
-        if (first) {
-#pragma unroll
-          for (int c = 0; c < NC; ++c) f.v[1][c] = 0.0;
-        } else if constexpr (COH) {
-          ld_node<NC>(xin2, off, f.v[1]);
-        } else {
-          ldg_node<NC>(xin2, off, f.v[1]);
-        }
-        if (!first && own && r >= J0 && r < J1) ld_node<NC>(a.xs + voff, off + i, f.xv);
-      }
+      ldg_node<NC>(xin, off, f.v[0]);
       if constexpr (HAS_DINV) ldg_node<NC>(dvin, off, f.dv);
     }
   };
@@ -372,21 +396,6 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
       if constexpr (HAS_DINV) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) S.dg[c] = f.dv[c];
-      }
-      if constexpr (ACT == PCGA) {
-        // z = M^-1 r with M^-1 = diag(1/D) (fem.py:303-305); p = z + beta p_old
-#pragma unroll
-        for (int c = 0; c < NC; ++c) v[c] = fma(beta, f.v[1][c], v[c] * f.dv[c]);
-        if (own && r >= J0 && r < J1) {
-          const int64_t node = (int64_t)r * nxp + i;
-          st_node<NC>(a.y2 + voff, node, v);
-          if (!first) {  // x_i = x_{i-1} + alpha_{i-1} p_{i-1} (moved here from pass B)
-            double xn[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) xn[c] = fma(alpha_prev, f.v[1][c], f.xv[c]);
-            st_node<NC>(a.xs + voff, node, xn);
-          }
-        }
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -429,10 +438,6 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
           part[2] += rv[c] * (rv[c] * S.dg[c]);
         }
         st_node<NC>(a.y + voff, node, rv);
-      } else if constexpr (ACT == PCGA) {
-        st_node<NC>(a.y + voff, node, yv);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) part[0] += S.raw[c] * yv[c];
       } else if constexpr (ACT == STATS) {
         double vv[NC];
         ldg_node<NC>(a.x2, node, vv);
@@ -502,65 +507,191 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
   }
 }
 
-template <class PH, int ACT, class W>
-__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
-  constexpr int NC = PH::NC;  // components per node of each input field
-  constexpr int NP = Traits<PH, ACT>::NP;
-  constexpr int NPA = NP > 0 ? NP : 1;
-  __shared__ double scratch[NPA * kWarps];
+// ----------------------------------------------------------------------------
+// Single-pass PCG iteration task (strip group bx, row segment by, rhs): the
+// marching skeleton above specialised for the PCG pass,
+//   r_i = r_{i-1} - alpha_{i-1} q_{i-1}, z = M^-1 r_i, p_i = z + beta_i p_{i-1}
+// on every node the task touches (halo nodes recompute their neighbours'
+// values bit for bit); owned nodes store r_i, p_i, q_i = A p_i and
+// x += alpha_{i-1} p_{i-1}, and sum p.q, z.q, q.M^-1 q, r.z, r.r.
+// The five inputs per node (r_{i-1}, p_{i-1}, q_{i-1}, M^-1 and, on owned
+// nodes, x) are prefetched into a register ring kPcgDepth rows deep: the
+// loads of rows r+1 and r+2 are in flight while row r is computed.  (A
+// shared-memory ring fed by per-thread cp.async, which frees those registers,
+// measured slower: 55.4 vs 55.9 us at cfg2 but 234 vs 210 us at cfg4.)
+// COH: the inputs were written earlier in the same launch (the persistent
+// kernel, across grid barriers): coherent loads instead of the read-only path.
+// ----------------------------------------------------------------------------
+constexpr int kPcgDepth = 3;   // node rows in the register ring
+constexpr int kPcgFields = 5;  // r, p, q, M^-1, x
 
+template <class PH, bool COH = false>
+__device__ __forceinline__ void march_pcg(const PH &ph, const Geo &g, const MArgs &a, int bx,
+                                          int by, int rhs, bool first, double beta,
+                                          double alpha_prev, double (&part)[5]) {
+  constexpr int NC = PH::NC, NOUT = PH::NOUT, D = kPcgDepth;
+  static_assert(PH::NIN == NC, "PCG operators read one field");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int strip = blockIdx.x * kWarps + warp;
-  const int rhs = blockIdx.z;
+  const int strip = bx * kWarps + warp;
+  const uint8_t *words = static_cast<const uint8_t *>(a.words);
   const int nx = g.nx, ny = g.ny;
   const int64_t nxp = nx + 1;
   const int64_t nn = nxp * (ny + 1);
-
   const int i = strip * kStrip - 1 + lane;
   const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
   const bool own = node_ok && lane >= 1 && lane <= kStrip;
   const int ic = min(max(i, 0), nx);  // clamped column: always a valid address
-  const int J0 = blockIdx.y * a.seg;
+  const int J0 = by * a.seg;
   const int J1 = min(J0 + a.seg, ny + 1);
-  const size_t voff = (ACT == SHAPE) ? 0 : (size_t)rhs * (size_t)nn * NC;
+  const size_t voff = (size_t)rhs * (size_t)nn * NC;
+  const double *r_in = a.x + voff, *p_in = a.x2 + voff, *q_in = a.x3 + voff;
 
-  double beta = 0.0, alpha_prev = 0.0;
-  bool first = false;
-  if constexpr (ACT == PCGA) {
-    lsg_pcg_scalars &s = a.scal[rhs];
-    if (s.done != 0.0 || a.finish_only) {  // uniform across the CTA
-      if (s.done == 0.0 || s.reserved[1] == 0.0) return;
-      // converged: apply the pending x += alpha p of its last iteration
-      const double al = s.alpha;
-      if (own) {
-        for (int r = J0; r < J1; ++r) {
-          const int64_t node = (int64_t)r * nxp + i;
-          double xo[NC], po[NC];
-          ld_node<NC>(a.xs + voff, node, xo);
-          ld_node<NC>(a.x2 + voff, node, po);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) xo[c] = fma(al, po[c], xo[c]);
-          st_node<NC>(a.xs + voff, node, xo);
-        }
-      }
-      double d1[1] = {0.0}, t1[1];
-      const int nblk = gridDim.x * gridDim.y;
-      if (block_partial_and_total<1, 0u>(d1, a.partials + (size_t)rhs * nblk,
-                                         a.counters + rhs, blockIdx.y * gridDim.x + blockIdx.x,
-                                         nblk, scratch, t1))
-        if (threadIdx.x == 0) s.reserved[1] = 0.0;
-      return;
+  struct Row {
+    double in[NC], rt[NC], raw[NC], dg[NC], z[NC];
+    uint32_t wc;
+  };
+  uint32_t wring[D];
+  double ring[D][kPcgFields][NC];
+  auto ldn = [&](const double *src, int64_t node, double *v) {
+    if constexpr (COH) ld_node<NC>(src, node, v);  // written earlier in this launch
+    else ldg_node<NC>(src, node, v);
+  };
+
+  auto fetch = [&](int r, int s) {
+    const int64_t node = (int64_t)r * nxp + ic;
+    wring[s] = node_ok ? (uint32_t)__ldg(words + node) : 0u;
+    ldn(r_in, node, ring[s][0]);
+    if (!first) {
+      ldn(p_in, node, ring[s][1]);
+      ldn(q_in, node, ring[s][2]);
     }
-    first = s.first != 0.0;
-    beta = s.beta;
-    alpha_prev = s.alpha;
-  } else if constexpr (ACT == RESID) {
-    if (a.scal[rhs].done != 0.0) return;
+    ldg_node<NC>(a.dinv, node, ring[s][3]);
+    if (!first && own && r >= J0 && r < J1) ld_node<NC>(a.xs + voff, node, ring[s][4]);
+  };
+
+  auto prepare = [&](int r, int s, Row &S) {
+    S.wc = wring[s];
+    const uint32_t m = PH::mask(S.wc);
+    double R[NC], P[NC], Q[NC], v[NC], rv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      R[c] = ring[s][0][c];
+      S.dg[c] = ring[s][3][c];
+      P[c] = ring[s][1][c];
+      Q[c] = ring[s][2][c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      rv[c] = first ? R[c] : fma(-alpha_prev, Q[c], R[c]);
+      S.z[c] = rv[c] * S.dg[c];  // M^-1 = diag(1/D) (fem.py:303-305)
+      v[c] = first ? S.z[c] : fma(beta, P[c], S.z[c]);
+    }
+    if (own && r >= J0 && r < J1) {
+      const int64_t node = (int64_t)r * nxp + i;
+      st_node<NC>(a.y3 + voff, node, rv);
+      st_node<NC>(a.y2 + voff, node, v);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        part[3] += rv[c] * S.z[c];
+        part[4] += rv[c] * rv[c];
+      }
+      if (!first) {  // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
+        double X[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) X[c] = fma(alpha_prev, P[c], ring[s][4][c]);
+        st_node<NC>(a.xs + voff, node, X);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      S.raw[c] = v[c];
+      S.in[c] = ((m >> c) & 1u) ? 0.0 : v[c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) S.rt[c] = __shfl_down_sync(0xffffffffu, S.in[c], 1);
+  };
+
+  auto emit = [&](int r, const Row &S, const double *accv) {
+    const int64_t node = (int64_t)r * nxp + i;
+    const uint32_t m = PH::mask(S.wc);
+    double yv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) yv[c] = ((m >> c) & 1u) ? S.raw[c] : accv[c];
+    st_node<NC>(a.y + voff, node, yv);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      part[0] += S.raw[c] * yv[c];
+      part[1] += S.z[c] * yv[c];
+      part[2] += yv[c] * (yv[c] * S.dg[c]);
+    }
+  };
+
+  auto step = [&](int r, int s, const Row &Sp, Row &Sn, double *ap, double *an) {
+    prepare(r, s, Sn);
+    double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
+    ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, i, r - 1, c00, c10, c01, c11);
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);
+      double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
+      if (lane == 0) up10 = up11 = 0.0;
+      ap[t] += c00[t] + up10;
+      an[t] = c01[t] + up11;
+    }
+    if (own && (r - 1) >= J0) emit(r - 1, Sp, ap);
+  };
+
+  const int jstart = max(J0 - 1, 0);
+  const int rend = min(J1, ny);
+  Row SA, SB;
+  double accA[NOUT], accB[NOUT];
+#pragma unroll
+  for (int s = 0; s < D; ++s) fetch(min(jstart + s, rend), s);
+  prepare(jstart, 0, SA);
+  fetch(min(jstart + D, rend), 0);
+#pragma unroll
+  for (int t = 0; t < NOUT; ++t) accA[t] = 0.0;
+  bool last_in_b = false;  // which register set holds row rend after the loop
+  int r = jstart + 1;      // row r lives in ring slot (r - jstart) % D
+  constexpr int U = (D % 2 == 0) ? D : 2 * D;  // ring slot and register-set parity both repeat
+  while (r <= rend) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (r <= rend) {
+        const int s = (u + 1) % D;
+        if (u % 2 == 0) step(r, s, SA, SB, accA, accB);
+        else step(r, s, SB, SA, accB, accA);
+        last_in_b = (u % 2 == 0);
+        fetch(min(r + D, rend), s);
+        ++r;
+      }
+    }
   }
+  if (J1 == ny + 1 && own && ny >= J0) {
+    if (last_in_b) emit(ny, SB, accB);
+    else emit(ny, SA, accA);
+  }
+}
+
+template <class PH, int ACT, class W>
+__global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
+  constexpr int NP = Traits<PH, ACT>::NP;
+  constexpr int NPA = NP > 0 ? NP : 1;
+  __shared__ double scratch[NPA * kWarps];
+  const int rhs = blockIdx.z;
   double part[NPA];
 #pragma unroll
   for (int t = 0; t < NPA; ++t) part[t] = 0.0;
-  march_core<PH, ACT, W>(ph, g, a, blockIdx.x, blockIdx.y, rhs, first, beta, alpha_prev, part);
+  if constexpr (ACT == PCG) {
+    const lsg_pcg_scalars &s = a.scal[rhs];
+    if (s.done != 0.0) return;  // uniform across the CTA (x is final: nothing pending)
+    march_pcg<PH>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.first != 0.0, s.beta, s.alpha, part);
+  } else {
+    if constexpr (ACT == RESID) {
+      if (a.scal[rhs].done != 0.0) return;
+    }
+    march_core<PH, ACT, W>(ph, g, a, blockIdx.x, blockIdx.y, rhs, part);
+  }
 
   if constexpr (NP > 0) {
     const int nblk = gridDim.x * gridDim.y;

@@ -1,6 +1,6 @@
-// 2D kernels of liblsgpu: operator apply and fused PCG passes (warp
-// marching, see march2d.cuh), fused compliance + shape-derivative RHS,
-// velocity statistics, material words and the PCG update pass.
+// 2D kernels of liblsgpu: operator apply and the single-pass PCG iteration
+// (warp marching, see march2d.cuh), fused compliance + shape-derivative RHS,
+// velocity statistics and material words.
 #include <math.h>
 #include <stdlib.h>
 
@@ -12,76 +12,7 @@
 namespace lsg {
 namespace d2 {
 
-// ----------------------------------------------------------------------------
-// PCG pass B (elementwise): x += alpha p ; r -= alpha q ; rz = r.M^-1 r ; rr.
-// Grid-stride over nodes with kUpd nodes in flight per thread: one wave of
-// CTAs per right-hand side, so the fixed-order final reduction stays short.
-// ----------------------------------------------------------------------------
 constexpr int kEwThreads = 256;
-constexpr int kUpd = 2;
-
-template <int NC>
-__global__ void __launch_bounds__(kEwThreads, 4)
-    pcg_update(int64_t nn, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
-               double *partials, uint32_t *counters) {
-  __shared__ double scratch[2 * (kEwThreads / 32)];
-  const int rhs = blockIdx.y;
-  lsg_pcg_scalars &s = scal[rhs];
-  if (s.done != 0.0) return;
-  const double alpha = s.alpha;
-  const size_t voff = (size_t)rhs * (size_t)nn * NC;
-  double *rv = r + voff;
-  const double *qv = q + voff;
-  const int64_t stride = (int64_t)gridDim.x * kEwThreads;
-  double part[2] = {0.0, 0.0};
-  for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < nn;
-       base += stride * kUpd) {
-    double Q[kUpd][NC], R[kUpd][NC], D[kUpd][NC];
-#pragma unroll
-    for (int u = 0; u < kUpd; ++u) {
-      const int64_t node = base + u * stride;
-      if (node < nn) {
-        ldg_node<NC>(qv, node, Q[u]);
-        ldg_node<NC>(dinv, node, D[u]);
-        ld_node<NC>(rv, node, R[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUpd; ++u) {
-      const int64_t node = base + u * stride;
-      if (node < nn) {
-        double ro[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          ro[c] = fma(-alpha, Q[u][c], R[u][c]);
-          part[0] += ro[c] * (ro[c] * D[u][c]);
-          part[1] += ro[c] * ro[c];
-        }
-        st_node<NC>(rv, node, ro);
-      }
-    }
-  }
-  double tot[2];
-  const int nblk = gridDim.x;
-  if (block_partial_and_total<2, 0u>(part, partials + (size_t)rhs * nblk * 2, counters + rhs,
-                                     blockIdx.x, nblk, scratch, tot)) {
-    if (threadIdx.x == 0) {
-      s.iters += 1.0;
-      s.rz_new = tot[0];
-      s.rr = tot[1];
-      s.reserved[1] = 1.0;  // x += alpha p of this iteration is pending (next pass A / finish)
-      if (sqrt(tot[1]) < s.atol) {
-        s.done = 1.0;
-      } else if (s.iters >= s.maxiter || !isfinite(tot[1]) || !isfinite(tot[0])) {
-        s.done = 2.0;  // iteration cap exhausted: SolverError on the host
-      } else {
-        s.beta = tot[0] / s.rho;
-        s.rho = tot[0];
-        s.first = 0.0;
-      }
-    }
-  }
-}
 
 // ----------------------------------------------------------------------------
 // Material words (levelset.py:65-67, models/base.py:117-119).
@@ -309,13 +240,6 @@ static dim3 march_grid(const Geo &g, int seg, int k) {
               (unsigned)k);
 }
 
-static int64_t upd_blocks(int64_t nn, int k) {
-  int64_t need = ceil_div(nn, (int64_t)kEwThreads * kUpd);
-  int64_t slots = (int64_t)kSMs * 4 / k;
-  if (slots < 1) slots = 1;
-  return need < slots ? need : slots;
-}
-
 int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 
 static Elast make_elast(const Geo &g, const lsg_op &op) {
@@ -370,6 +294,8 @@ static int launch_march(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march<PH, ACT, uint8_t>,
                                                       kThreads, 0) != cudaSuccess)
       ctas_per_sm = 4;
+    const char *e = getenv("LSG_M2_GRID_CTAS");  // experiment: size the grid for this many
+    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
   }
   a.seg = seg_for(g, k, ctas_per_sm);
   a.nstrips = nstrips_of(g);
@@ -466,41 +392,35 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
 
 
 // ----------------------------------------------------------------------------
-// Persistent PCG (2D): all `niter` iterations of pass A + pass B in one
-// cooperative launch, two grid-wide barriers per iteration instead of two
-// kernel boundaries.  Every CTA keeps the per-RHS scalars in shared memory
-// and forms the alpha / beta reductions itself from the per-CTA partials in
-// one fixed order, so all CTAs take identical decisions (and the results are
-// deterministic); CTA 0 mirrors the scalars to global memory.  Same algorithm
-// and stopping rule as the two-kernel path (march<.., PCGA> + pcg_update).
+// Persistent PCG (2D): all `niter` single-pass iterations in one cooperative
+// launch, one grid-wide barrier per iteration instead of one kernel boundary.
+// Every CTA keeps the per-RHS scalars in shared memory and reduces the per-CTA
+// partials itself in one fixed order, so all CTAs take identical decisions
+// (deterministic results); CTA 0 mirrors the scalars to global memory.  Same
+// algorithm and stopping rule as march<.., PCG> (pcg_decide).  The partials
+// alternate between two buffers by iteration: a CTA still reading iteration
+// i's sums cannot be overtaken by a writer of iteration i+2 (barrier i+1).
 // ----------------------------------------------------------------------------
 namespace cgrp = cooperative_groups;
+
+constexpr int kPcgSums = Traits<Elast, PCG>::NP;  // p.q, z.q, q.M^-1 q, r.z, r.r
 
 template <class PH, int KMAX>
 __global__ void __launch_bounds__(kThreads)
     pcg_persistent(PH ph, Geo g, MArgs a, int k, int tx, int ty, int niter, int parity0,
-                   double *p_even, double *p_odd, double *pbuf) {
-  constexpr int NC = PH::NC;
+                   double *r_even, double *r_odd, double *p_even, double *p_odd, double *q_even,
+                   double *q_odd, double *pbuf) {
+  constexpr int NS = kPcgSums;
+  constexpr int G = KMAX >= 2 ? 2 : 1;  // right-hand sides per block reduction
   cgrp::grid_group grid = cgrp::this_grid();
-  __shared__ double scratch[2 * KMAX * kWarps];
-  __shared__ double s_beta[KMAX], s_alpha[KMAX], s_rho[KMAX], s_atol[KMAX], s_iters[KMAX];
-  __shared__ double s_maxit[KMAX], s_pa[KMAX];
-  __shared__ int s_first[KMAX], s_done[KMAX], s_newly[KMAX], s_all;
-  const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
+  __shared__ double scratch[NS * G * kWarps];
+  __shared__ lsg_pcg_scalars s_sc[KMAX];
+  __shared__ double s_part[KMAX * NS];
+  __shared__ int s_all;
   const int ncta = gridDim.x, cta = blockIdx.x;
-  double *pa = pbuf, *pb = pbuf + (size_t)ncta * KMAX;  // [ncta][KMAX], [ncta][2 KMAX]
-  if (threadIdx.x < KMAX) {
-    const int r = threadIdx.x;
-    const bool live = r < k;
-    const lsg_pcg_scalars &sc = a.scal[live ? r : 0];
-    s_beta[r] = sc.beta;
-    s_alpha[r] = sc.alpha;
-    s_rho[r] = sc.rho;
-    s_atol[r] = sc.atol;
-    s_iters[r] = sc.iters;
-    s_maxit[r] = sc.maxiter;
-    s_first[r] = sc.first != 0.0;
-    s_done[r] = live ? (sc.done != 0.0) : 1;
+  for (int t = threadIdx.x; t < KMAX; t += kThreads) {
+    if (t < k) s_sc[t] = a.scal[t];
+    else s_sc[t].done = 1.0;
   }
   __syncthreads();
   int parity = parity0;
@@ -508,140 +428,57 @@ __global__ void __launch_bounds__(kThreads)
   for (int it = 0; it < niter; ++it, parity ^= 1) {
     if (threadIdx.x == 0) {
       int all = 1;
-      for (int r = 0; r < KMAX; ++r) all &= s_done[r];
+      for (int r = 0; r < KMAX; ++r) all &= s_sc[r].done != 0.0;
       s_all = all;
     }
+    for (int t = threadIdx.x; t < KMAX * NS; t += kThreads) s_part[t] = 0.0;
     __syncthreads();
-    if (s_all) continue;  // identical in every CTA: no barrier is skipped by only some
+    if (s_all) break;  // identical in every CTA: no barrier is skipped by only some
     MArgs aa = a;
-    aa.x2 = parity ? p_odd : p_even;  // p_old
-    aa.y2 = parity ? p_even : p_odd;  // p_new
-    // pass A: p = M^-1 r + beta p_old, q = A p, p.q partials, pending x update
-    if (threadIdx.x < KMAX) {
-      s_pa[threadIdx.x] = 0.0;
-      s_newly[threadIdx.x] = 0;
-    }
-    __syncthreads();
+    aa.x = parity ? r_odd : r_even;  // r_{i-1}
+    aa.y3 = parity ? r_even : r_odd;  // r_i
+    aa.x2 = parity ? p_odd : p_even;
+    aa.y2 = parity ? p_even : p_odd;
+    aa.x3 = parity ? q_odd : q_even;
+    aa.y = parity ? q_even : q_odd;
     for (int t = cta; t < ntask; t += ncta) {
       const int rhs = t / (tx * ty), rem = t - rhs * (tx * ty);
-      if (s_done[rhs]) continue;
-      double part[1] = {0.0};
-      march_core<PH, PCGA, uint8_t, true>(ph, g, aa, rem % tx, rem / tx, rhs, s_first[rhs] != 0,
-                                   s_beta[rhs], s_alpha[rhs], part);
-      block_reduce<1, 0u>(part, scratch);
-      if (threadIdx.x == 0) s_pa[rhs] += part[0];
+      const lsg_pcg_scalars &sc = s_sc[rhs];
+      if (sc.done != 0.0) continue;
+      double part[NS];
+#pragma unroll
+      for (int v = 0; v < NS; ++v) part[v] = 0.0;
+      march_pcg<PH, true>(ph, g, aa, rem % tx, rem / tx, rhs, sc.first != 0.0, sc.beta, sc.alpha,
+                          part);
+      block_reduce<NS, 0u>(part, scratch);
+      if (threadIdx.x == 0)
+#pragma unroll
+        for (int v = 0; v < NS; ++v) s_part[rhs * NS + v] += part[v];
       __syncthreads();
     }
-    if (threadIdx.x < KMAX) pa[(size_t)cta * KMAX + threadIdx.x] = s_pa[threadIdx.x];
+    double *pw = pbuf + (size_t)(it & 1) * ncta * KMAX * NS;
+    for (int t = threadIdx.x; t < KMAX * NS; t += kThreads) pw[(size_t)cta * KMAX * NS + t] = s_part[t];
     grid.sync();
-    {  // alpha = rho / p.q, all RHS in one fixed-order reduction (same in every CTA)
-      double acc[KMAX];
+    // every CTA: the same fixed-order sums over all CTAs, then the same decisions
+    for (int r0 = 0; r0 < k; r0 += G) {
+      double acc[G * NS];
 #pragma unroll
-      for (int r = 0; r < KMAX; ++r) acc[r] = 0.0;
+      for (int v = 0; v < G * NS; ++v) acc[v] = 0.0;
       for (int c = threadIdx.x; c < ncta; c += kThreads)
 #pragma unroll
-        for (int r = 0; r < KMAX; ++r) acc[r] += __ldcg(pa + (size_t)c * KMAX + r);
-      block_reduce<KMAX, 0u>(acc, scratch);
+        for (int v = 0; v < G * NS; ++v)
+          if (r0 * NS + v < KMAX * NS) acc[v] += __ldcg(pw + (size_t)c * KMAX * NS + r0 * NS + v);
+      block_reduce<G * NS, 0u>(acc, scratch);
       if (threadIdx.x == 0) {
-        for (int r = 0; r < k; ++r) {
-          if (s_done[r]) continue;
-          s_alpha[r] = s_rho[r] / acc[r];
-          if (cta == 0) a.scal[r].pq = acc[r];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          const int r = r0 + gg;
+          if (r >= k || s_sc[r].done != 0.0) continue;
+          pcg_decide(s_sc[r], acc + gg * NS);
+          if (cta == 0) a.scal[r] = s_sc[r];
         }
       }
       __syncthreads();
-    }
-    // pass B: r -= alpha q ; r.M^-1 r ; r.r
-    double part[2 * KMAX];
-#pragma unroll
-    for (int r = 0; r < 2 * KMAX; ++r) part[r] = 0.0;
-#pragma unroll
-    for (int r = 0; r < KMAX; ++r) {
-      if (r >= k || s_done[r]) continue;
-      const double alpha = s_alpha[r];
-      double *rv = const_cast<double *>(a.x) + (size_t)r * nn * NC;  // r (pass A reads it as x)
-      const double *qv = a.y + (size_t)r * nn * NC;
-      for (int64_t node = (int64_t)cta * kThreads + threadIdx.x; node < nn;
-           node += (int64_t)ncta * kThreads) {
-        double Q[NC], R[NC], D[NC];
-        ld_node<NC>(qv, node, Q);  // written by pass A of this launch: coherent load
-        ldg_node<NC>(a.dinv, node, D);
-        ld_node<NC>(rv, node, R);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          R[c] = fma(-alpha, Q[c], R[c]);
-          part[2 * r] += R[c] * (R[c] * D[c]);
-          part[2 * r + 1] += R[c] * R[c];
-        }
-        st_node<NC>(rv, node, R);
-      }
-    }
-    block_reduce<2 * KMAX, 0u>(part, scratch);
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int r = 0; r < 2 * KMAX; ++r) pb[(size_t)cta * 2 * KMAX + r] = part[r];
-    grid.sync();
-    {
-      double acc[2 * KMAX];
-#pragma unroll
-      for (int r = 0; r < 2 * KMAX; ++r) acc[r] = 0.0;
-      for (int c = threadIdx.x; c < ncta; c += kThreads)
-#pragma unroll
-        for (int r = 0; r < 2 * KMAX; ++r) acc[r] += __ldcg(pb + (size_t)c * 2 * KMAX + r);
-      block_reduce<2 * KMAX, 0u>(acc, scratch);
-      if (threadIdx.x == 0) {
-        for (int r = 0; r < k; ++r) {
-          if (s_done[r]) continue;
-          const double rz = acc[2 * r], rr = acc[2 * r + 1];
-          s_iters[r] += 1.0;
-          int done = 0;
-          if (sqrt(rr) < s_atol[r]) done = 1;
-          else if (s_iters[r] >= s_maxit[r] || !isfinite(rr) || !isfinite(rz)) done = 2;
-          else {
-            s_beta[r] = rz / s_rho[r];
-            s_rho[r] = rz;
-            s_first[r] = 0;
-          }
-          s_done[r] = done != 0;
-          s_newly[r] = done != 0;
-          if (cta == 0) {
-            lsg_pcg_scalars &sc = a.scal[r];
-            sc.iters = s_iters[r];
-            sc.rz_new = rz;
-            sc.rr = rr;
-            // x += alpha p of this iteration: folded into the next pass A while the
-            // RHS runs, applied just below (in this launch) once it has stopped
-            sc.reserved[1] = done ? 0.0 : 1.0;
-            sc.alpha = s_alpha[r];
-            if (done) sc.done = (double)done;
-            else {
-              sc.beta = s_beta[r];
-              sc.rho = s_rho[r];
-              sc.first = 0.0;
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-    // right-hand sides that stopped in this iteration: their last x += alpha p now,
-    // while p_new still holds their last direction (later iterations flip the
-    // buffers; no other pass touches their x again)
-#pragma unroll
-    for (int r = 0; r < KMAX; ++r) {
-      if (!s_newly[r]) continue;
-      const double alpha = s_alpha[r];
-      double *xv = a.xs + (size_t)r * nn * NC;
-      const double *pv = aa.y2 + (size_t)r * nn * NC;
-      for (int64_t node = (int64_t)cta * kThreads + threadIdx.x; node < nn;
-           node += (int64_t)ncta * kThreads) {
-        double X[NC], P[NC];
-        ld_node<NC>(xv, node, X);
-        ld_node<NC>(pv, node, P);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) X[c] = fma(alpha, P[c], X[c]);
-        st_node<NC>(xv, node, X);
-      }
     }
   }
 }
@@ -667,21 +504,22 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
   if (per_sm <= 0) return 1;  // not launchable cooperatively: caller falls back
   static int ctas_march = -1;
   if (ctas_march < 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_march, march<PH, PCGA, uint8_t>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_march, march<PH, PCG, uint8_t>,
                                                     kThreads, 0) != cudaSuccess)
     ctas_march = 4;
   a.seg = seg_for(g, ws.k, ctas_march);
   a.nstrips = nstrips_of(g);
   const dim3 mg = march_grid(g, a.seg, ws.k);
   const int ntask = (int)(mg.x * mg.y * ws.k);
-  // one task per CTA where possible, at least one CTA per SM for pass B
+  // one task per CTA where possible, at least one CTA per SM for the loads
   int ncta = ntask < kSMs ? kSMs : ntask;
   if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
   int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
-  double *pe = ws.p, *po = ws.p_alt, *pbuf = ws.partials;
+  double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
+  double *pbuf = ws.partials;
   PH phc = ph;
   Geo gc = g;
-  void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &pe, &po, &pbuf};
+  void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &re, &ro, &pe, &po, &qe, &qo, &pbuf};
   if (cudaLaunchCooperativeKernel((void *)pcg_persistent<PH, KMAX>, dim3((unsigned)ncta),
                                   dim3(kThreads), args, 0, st) != cudaSuccess)
     return check_launch("pcg_persistent");
@@ -714,7 +552,6 @@ bool pcg_persistent_ok(const lsg_op &op, const lsg_pcg_ws &ws) {
 
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
-  const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
   MArgs a = {};
   a.words = op.words;
   a.x = ws.r;
@@ -731,42 +568,24 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     else rc = launch_persistent<Lap>(make_lap(g, op), g, a, ws, niter, st);
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = not cooperative, fall through
   }
-  const dim3 eg((unsigned)upd_blocks(nn, ws.k), (unsigned)ws.k);
   for (int it = 0; it < niter; ++it) {
-    double *p_old = ws.parity ? ws.p_alt : ws.p;
-    double *p_new = ws.parity ? ws.p : ws.p_alt;
-    a.x2 = p_old;
-    a.y2 = p_new;
-    int rc = dispatch_op<PCGA>(op, a, ws.k, st);
-    if (rc) return rc;
-    if (nc_of(op) == 1)
-      pcg_update<1><<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
-                                               ws.counters);
-    else
-      pcg_update<2><<<eg, kEwThreads, 0, st>>>(nn, ws.dinv, ws.r, ws.q, ws.scal, ws.partials,
-                                               ws.counters);
-    rc = check_launch("pcg_update2d");
+    const bool odd = ws.parity != 0;
+    a.x = odd ? ws.r_alt : ws.r;  // r, p, q of the previous iteration ...
+    a.x2 = odd ? ws.p_alt : ws.p;
+    a.x3 = odd ? ws.q_alt : ws.q;
+    a.y3 = odd ? ws.r : ws.r_alt;  // ... and of this one
+    a.y2 = odd ? ws.p : ws.p_alt;
+    a.y = odd ? ws.q : ws.q_alt;
+    int rc = dispatch_op<PCG>(op, a, ws.k, st);
     if (rc) return rc;
     ws.parity ^= 1;
   }
   return LSG_OK;
 }
 
-// Apply the pending x += alpha p of right-hand sides that converged in the
-// last iteration they ran (the update is otherwise folded into pass A).
-int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
-  MArgs a = {};
-  a.words = op.words;
-  a.x = ws.r;
-  a.x2 = ws.parity ? ws.p_alt : ws.p;
-  a.scal = ws.scal;
-  a.partials = ws.partials;
-  a.counters = ws.counters;
-  a.dinv = ws.dinv;
-  a.xs = ws.x;
-  a.finish_only = 1;
-  return dispatch_op<PCGA>(op, a, ws.k, st);
-}
+// The single-pass iteration leaves nothing pending in 2D: x_i is formed in the
+// pass that tests r_i, so a right-hand side stops with its final x.
+int pcg_finish(const lsg_op &, lsg_pcg_ws &, cudaStream_t) { return LSG_OK; }
 
 template <int KB>
 static int shape_chunk(const Geo &g, const lsg_op &op, const double *u, double volume, double *vc,

@@ -284,15 +284,18 @@ class _Workspace:
         self.p = torch.empty((k, n), **dev)
         self.q = torch.empty((k, n), **dev)
         self.p_alt = torch.empty((k, n), **dev)
-        self.p_ring = torch.empty((k, n), **dev)
+        self.p_ring = torch.empty((k, n), **dev) if grid.dim == 3 else torch.empty(0, **dev)
+        self.r_alt = torch.empty((k, n), **dev) if grid.dim == 2 else torch.empty(0, **dev)
+        self.q_alt = torch.empty((k, n), **dev) if grid.dim == 2 else torch.empty(0, **dev)
         self.scal = torch.zeros((k, _lib.SCAL_DOUBLES), **dev)
         npart = int(_lib.load().lsg_partials_per_rhs(grid))
-        self.partials = torch.zeros(k * npart * 4, **dev)
+        self.partials = torch.zeros(k * npart * 8, **dev)
         self.counters = torch.zeros(max(k, 1), dtype=torch.int32, device="cuda")
         self.host_scal = torch.zeros((k, _lib.SCAL_DOUBLES), dtype=torch.float64, pin_memory=True)
         self.ws = _lib.PcgWs()
         self.ws.k = k
-        for name in ("x", "b", "r", "p", "q", "scal", "partials", "counters", "p_alt", "p_ring"):
+        for name in ("x", "b", "r", "p", "q", "scal", "partials", "counters", "p_alt", "p_ring",
+                     "r_alt", "q_alt"):
             setattr(self.ws, name, getattr(self, name).data_ptr())
 
 

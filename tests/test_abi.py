@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol():
 
 def test_host_only_entry_points():
     lib = _lib.load(require_device=False)
-    assert lib.lsg_abi_version() == 2
+    assert lib.lsg_abi_version() == 3
     g = _lib.make_grid(2, (160, 80), (0.0, 0.0), (2.0, 1.0))
     assert lib.lsg_num_nodes(g) == 161 * 81
     assert lib.lsg_num_elements(g) == 2 * 160 * 80
