@@ -267,16 +267,20 @@ def b200_arm(args, world, rank, local):
     op = opt.model.operator(opt.phi)
     u = torch.randn((k, d * N), dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    times = []
+    # queued behind a device sleep: the events bracket device time, not the host launch
+    torch.cuda.synchronize()
+    torch.cuda._sleep(100_000_000)
+    evs = []
     for rep in range(23):
         flush.fill_(float(rep))
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         op.apply(u)
         a1.record(stream)
-        torch.cuda.synchronize()
         if rep >= 3:
-            times.append(a0.elapsed_time(a1) / 1e3)
+            evs.append((a0, a1))
+    torch.cuda.synchronize()
+    times = [a0.elapsed_time(a1) / 1e3 for a0, a1 in evs]
     t_apply = statistics.median(times)
     apply_bytes = 16.0 * d * k * N + E
     del flush

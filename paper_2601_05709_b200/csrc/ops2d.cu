@@ -223,8 +223,8 @@ static int nstrips_of(const Geo &g) { return (int)ceil_div(g.nx + 1, kStrip); }
 constexpr int kSMs = 148;
 constexpr int kMaxPartials = 4096;  // >= CTAs per rhs of any launch below
 
-static int seg_for(const Geo &g, int k, int ctas_per_sm) {
-  const int64_t cols = ceil_div(nstrips_of(g), kWarps);
+static int seg_for(const Geo &g, int k, int ctas_per_sm, int nstrips = -1, int warps = kWarps) {
+  const int64_t cols = ceil_div(nstrips < 0 ? nstrips_of(g) : nstrips, warps);
   const int64_t rows = g.ny + 1;
   int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 4);
   int64_t nseg = slots / (cols * k);
@@ -302,6 +302,82 @@ static int launch_march(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t
   const dim3 grid = march_grid(g, a.seg, k);
   march<PH, ACT, uint8_t><<<grid, kThreads, 0, st>>>(ph, g, a);
   return check_launch("march2d");
+}
+
+// The recompute-q PCG pass: 28-column strips, its own occupancy-sized grid.
+// LSG_PCG2D_RQ: 0 = stored-q pass (march_pcg), 1 = recompute pass with a
+// register prefetch ring (march_pcg_rq), 2 = with the shared-memory cp.async
+// ring (march_pcg_rqs, default), 3 = software-pipelined with the whole row state in a
+// shared-memory ring (march_pcg_rqp).
+static int pcg_rq_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_PCG2D_RQ");
+    v = e ? atoi(e) : 2;
+    if (v < 0 || v > 3) v = 3;
+  }
+  return v;
+}
+
+template <class PH, bool SMEM>
+static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  static int ctas_per_sm = -1;
+  if (ctas_per_sm < 0) {
+    const cudaError_t e0 =
+        SMEM ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH>, kThreads, 0)
+             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rq_kernel<PH>, kThreads, 0);
+    if (e0 != cudaSuccess) ctas_per_sm = 3;
+    const char *e = getenv("LSG_M2_GRID_CTAS");
+    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
+  }
+  a.nstrips = (int)ceil_div(g.nx + 1, kStripRq);
+  a.seg = seg_for(g, k, ctas_per_sm, a.nstrips);
+  const dim3 grid((unsigned)ceil_div(a.nstrips, kWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
+                  (unsigned)k);
+  if (SMEM) march_pcg_rqs_kernel<PH><<<grid, kThreads, 0, st>>>(ph, g, a);
+  else march_pcg_rq_kernel<PH><<<grid, kThreads, 0, st>>>(ph, g, a);
+  return check_launch("march2d_pcg_rq");
+}
+
+template <class PH>
+static int launch_pcg_rqp(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  constexpr int threads = kRqpWarps * 32;
+  const size_t smem = sizeof(double) * kRqpWarps * RqpRing<PH::NC>::WARP;
+  static int ctas_per_sm = -1;
+  if (ctas_per_sm < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqp_kernel<PH>, threads,
+                                                      smem) != cudaSuccess)
+      ctas_per_sm = 8;
+    const char *e = getenv("LSG_M2_GRID_CTAS");
+    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
+  }
+  a.nstrips = (int)ceil_div(g.nx + 1, kStripRq);
+  a.seg = seg_for(g, k, ctas_per_sm, a.nstrips, kRqpWarps);
+  const dim3 grid((unsigned)ceil_div(a.nstrips, kRqpWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
+                  (unsigned)k);
+  march_pcg_rqp_kernel<PH><<<grid, threads, smem, st>>>(ph, g, a);
+  return check_launch("march2d_pcg_rqp");
+}
+
+static int dispatch_pcg_rq(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
+  const Geo g = geo_of(op.grid);
+  if (pcg_rq_mode() == 3) {
+    if (op.kind == LSG_OP_ELASTICITY) return launch_pcg_rqp<Elast>(make_elast(g, op), g, a, k, st);
+    if (op.kind == LSG_OP_H1) return launch_pcg_rqp<H1>(make_h1(g, op), g, a, k, st);
+    if (op.kind == LSG_OP_LAPLACE) return launch_pcg_rqp<Lap>(make_lap(g, op), g, a, k, st);
+  }
+  const bool sm = pcg_rq_mode() == 2;
+  if (op.kind == LSG_OP_ELASTICITY)
+    return sm ? launch_pcg_rq<Elast, true>(make_elast(g, op), g, a, k, st)
+              : launch_pcg_rq<Elast, false>(make_elast(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_H1)
+    return sm ? launch_pcg_rq<H1, true>(make_h1(g, op), g, a, k, st)
+              : launch_pcg_rq<H1, false>(make_h1(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_LAPLACE)
+    return sm ? launch_pcg_rq<Lap, true>(make_lap(g, op), g, a, k, st)
+              : launch_pcg_rq<Lap, false>(make_lap(g, op), g, a, k, st);
+  set_error("unknown operator kind %d", op.kind);
+  return LSG_ERR_ARG;
 }
 
 template <int ACT>
@@ -386,6 +462,10 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   a.dinv = ws.dinv;
   rc = dispatch_op<RESID>(op, a, ws.k, st);
   if (rc) return rc;
+  // p_{-1} = 0 (the buffer the first pass reads as p_{i-1}): with alpha_{-1} =
+  // beta_0 = 0 the recompute pass needs no first-iteration branch
+  if (cudaMemsetAsync(ws.p, 0, sizeof(double) * (size_t)n * ws.k, st) != cudaSuccess)
+    return check_launch("memset p");
   zero_if_flag<<<dim3(64, ws.k), 256, 0, st>>>(n, ws.scal, ws.x);
   return check_launch("zero_if_flag");
 }
@@ -576,7 +656,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     a.y3 = odd ? ws.r : ws.r_alt;  // ... and of this one
     a.y2 = odd ? ws.p : ws.p_alt;
     a.y = odd ? ws.q : ws.q_alt;
-    int rc = dispatch_op<PCG>(op, a, ws.k, st);
+    int rc = pcg_rq_mode() ? dispatch_pcg_rq(op, a, ws.k, st) : dispatch_op<PCG>(op, a, ws.k, st);
     if (rc) return rc;
     ws.parity ^= 1;
   }

@@ -1,6 +1,7 @@
 """The three ways a 2D PCG chunk can run -- the persistent cooperative kernel
 (small systems), the CUDA-graph replay of the two-kernel iteration, and
-direct launches -- give the same solutions, including right-hand sides that
+direct launches, and the stored-q variant of the single pass
+(LSG_PCG2D_RQ=0) beside the default one that recomputes q_{i-1} -- give the same solutions, including right-hand sides that
 converge in the middle of a chunk (their pending x updates are applied by the
 next pass A or by lsg_pcg_finish).  Each path runs in its own process because
 the switches are read once per process.  Needs a B200."""
@@ -67,11 +68,42 @@ def test_pcg_paths_agree(tmp_path):
     xp, itp, tp = run_path(tmp_path, "persistent", {})
     xg, itg, tg = run_path(tmp_path, "graph", {"LSG_PCG2D_PERSISTENT": "0"})
     xd, itd, td = run_path(tmp_path, "direct", {"LSG_PCG2D_PERSISTENT": "0", "LSG_NO_GRAPHS": "1"})
-    for x, res in (tp, tg, td):  # every path meets the stopping rule in the true residual
+    xq, itq, tq = run_path(tmp_path, "storedq", {"LSG_PCG2D_PERSISTENT": "0", "LSG_PCG2D_RQ": "0"})
+    for x, res in (tp, tg, td, tq):  # every path meets the stopping rule in the true residual
         assert (res <= 1e-10).all(), res
     assert np.linalg.norm(tp[0] - tg[0]) <= 1e-10 * np.linalg.norm(tg[0])
     assert itp[2] == itg[2] == itd[2] == 0 and not xp[2].any() and not xg[2].any()
     assert itg == itd and np.array_equal(xg, xd)  # same kernels, same order: bitwise
+    # recomputed q_{i-1} is bit-identical to the stored one; only the grouping of
+    # the per-thread partial sums differs (28- vs 30-column strips)
+    assert itq[2] == 0 and not xq[2].any()
+    for r in range(2):
+        assert abs(itq[r] - itg[r]) <= max(2, itg[r] // 50)
+        assert np.linalg.norm(xq[r] - xg[r]) <= 1e-8 * np.linalg.norm(xg[r])
     for r in range(2):
         assert itp[r] > 10 and abs(itp[r] - itg[r]) <= max(2, itp[r] // 20)
         assert np.linalg.norm(xp[r] - xg[r]) <= 1e-8 * np.linalg.norm(xg[r])
+
+
+SWEEP = r"""
+import sys
+sys.path.insert(0, %(root)r)
+sys.path.insert(0, %(tests)r)
+import test_gpu_shapes as t
+for n in t.SHAPES_2D + [(7, 40), (33, 61)]:
+    t.test_shapes_2d(n)
+print("ok")
+"""
+
+
+def test_shape_sweep_graph_paths(tmp_path):
+    """The 2D grid-shape sweep (state PCG, velocity CG) with the persistent
+    kernel off, so every solve runs the per-launch single pass: the default
+    recompute-q pass (28-column strips, two halo rows per segment) and the
+    stored-q pass, on grids around every tile edge and with many row segments."""
+    script = tmp_path / "sweep.py"
+    script.write_text(SWEEP % {"root": ROOT, "tests": os.path.join(ROOT, "tests")})
+    for env in ({"LSG_PCG2D_PERSISTENT": "0"}, {"LSG_PCG2D_PERSISTENT": "0", "LSG_PCG2D_RQ": "0"}):
+        res = subprocess.run([sys.executable, str(script)], env=dict(os.environ, **env),
+                             capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0 and res.stdout.strip().endswith("ok"), (env, res.stderr[-3000:])

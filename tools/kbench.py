@@ -47,7 +47,12 @@ def main():
     out = {"grid": args.grid, "k": k, "nodes": N}
 
     def timed(fn, reps, flush_l2):
-        ts = []
+        # The whole sequence is queued behind a ~50 ms device sleep so that
+        # the GPU never waits on the host between e0 and the kernel: the
+        # events bracket device time only (not the Python/ctypes launch).
+        torch.cuda.synchronize()
+        torch.cuda._sleep(100_000_000)
+        evs = []
         for rep in range(reps + 3):
             if flush_l2:
                 flush.fill_(float(rep))
@@ -55,10 +60,10 @@ def main():
             e0.record(stream)
             fn()
             e1.record(stream)
-            torch.cuda.synchronize()
             if rep >= 3:
-                ts.append(e0.elapsed_time(e1) * 1e3)
-        return float(np.median(ts))
+                evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) * 1e3 for a, b in evs]))
 
     u = torch.randn((k, d * N), dtype=torch.float64, device="cuda")
     y = torch.empty_like(u)
