@@ -680,239 +680,37 @@ __device__ __forceinline__ void march_pcg(const PH &ph, const Geo &g, const MArg
 // is not read back from memory: the pass re-applies the operator to p_{i-1},
 // which it reads anyway to form p_i, so per right-hand side and iteration it
 // moves 6 vectors (reads r, p, x; writes r, p, x) instead of 8.  The extra
-// stencil costs ~45 fp64 instructions per cell, far below the memory time of
-// a 2D node (the pass stays HBM-bound).  q_{i-1} at a node is summed by the
-// same code in the same order as when it was q_i of the previous pass, so it
-// is bit-identical to the stored value and r_i is unchanged.
+// stencil costs ~45 fp64 instructions per cell.  q_{i-1} at a node is summed
+// by the same code in the same order wherever it is recomputed (owner or halo
+// warp), so every warp forms the same r_i, z_i, p_i of a node.
 //
 // Two stencils run one row apart: at step r the old stencil closes
 // q_{i-1} of row r-1, that row's r_i / z_i / p_i are formed (and r_i, p_i,
 // x_i stored on owned nodes), and the new stencil closes q_i of row r-2,
 // whose sums p.q, z.q, q.M^-1 q are taken.  Halo: two columns each side (a
 // warp owns lanes 2..29: kStripRq columns) and two rows below each segment.
-// Register rings (3 rows each): p_{i-1} + word for the old stencil (2 rows
-// ahead), r_{i-1}, M^-1, x for the forming step (lags one row).
+//
+// Iteration 0 needs no special case: pcg_start zeroes the p_{-1} buffer and
+// alpha_{-1} = beta_0 = 0, so r_0 - 0 q, 0 p + z and x + 0 p are exact.
+//
+// Prefetch ring in shared memory: every lane copies its own node of each
+// source row (p_{i-1}, r_{i-1}, M^-1, x; 16-byte cp.async; word: the aligned
+// 4-byte chunk that holds it) A rows ahead and reads back only what it copied
+// itself, so per-thread cp.async.wait_group orders the ring (no barriers).
+// Against register rings this frees ~48 registers (4 instead of 3 CTAs/SM).
+// A = 3 measured best on small batched grids (cfg2: 51.6 vs 52.5 us), A = 2
+// on large ones (cfg4: 183 vs 198 us).  (Also measured and removed: the register ring,
+// 52.9 / 185 us; a software-pipelined variant whose two stencils overlap as
+// independent chains with all row state in the ring, 57.3 / 204 us; keeping
+// the masked inputs in registers, 79 / 254 us.)
 // ----------------------------------------------------------------------------
 constexpr int kStripRq = 28;
 
-// Iteration 0 needs no special case: pcg_start zeroes the p_{-1} buffer and
-// alpha_{-1} = beta_0 = 0, so r_0 - 0 q, 0 p + z and x + 0 p are exact.
-template <class PH>
-__device__ __forceinline__ void march_pcg_rq(const PH &ph, const Geo &g, const MArgs &a, int bx,
-                                             int by, int rhs, double beta, double alpha_prev,
-                                             double (&part)[5]) {
-  constexpr int NC = PH::NC, NOUT = PH::NOUT, D = 3;
-  static_assert(PH::NIN == NC, "PCG operators read one field");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int strip = bx * kWarps + warp;
-  const uint8_t *words = static_cast<const uint8_t *>(a.words);
-  const int nx = g.nx, ny = g.ny;
-  const int64_t nxp = nx + 1;
-  const int64_t nn = nxp * (ny + 1);
-  const int i = strip * kStripRq - 2 + lane;
-  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
-  const bool own = node_ok && lane >= 2 && lane <= kStripRq + 1;
-  const int ic = min(max(i, 0), nx);
-  const int J0 = by * a.seg;
-  const int J1 = min(J0 + a.seg, ny + 1);
-  const size_t voff = (size_t)rhs * (size_t)nn * NC;
-  const double *r_in = a.x + voff, *p_in = a.x2 + voff;
-  double *xs = a.xs + voff;
-
-  // Rows keep only the raw value and the word; the masked operator input and
-  // its right neighbour are re-derived where a cell row uses them (keeping
-  // them measured 50% slower: register-capped code)
-  struct Old {  // p_{i-1} row
-    double raw[NC];
-    uint32_t wc;
-  };
-  struct New {  // p_i row
-    double raw[NC], z[NC], dg[NC];
-    uint32_t wc;
-  };
-  // masked operator input and its right neighbour (one shuffle) of a row
-  auto derive = [&](const double *raw, uint32_t wc, double *in, double *rt) {
-    const uint32_t m = PH::mask(wc);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) in[c] = ((m >> c) & 1u) ? 0.0 : raw[c];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) rt[c] = __shfl_down_sync(0xffffffffu, in[c], 1);
-  };
-  uint32_t wring[D];
-  double pring[D][NC];
-  double fring[D][3][NC];  // r_{i-1}, M^-1, x
-
-  auto fetch_p = [&](int r, int s) {
-    const int64_t node = (int64_t)r * nxp + ic;
-    wring[s] = node_ok ? (uint32_t)__ldg(words + node) : 0u;
-    ldg_node<NC>(p_in, node, pring[s]);
-  };
-  auto fetch_f = [&](int r, int s) {
-    const int64_t node = (int64_t)r * nxp + ic;
-    ldg_node<NC>(r_in, node, fring[s][0]);
-    ldg_node<NC>(a.dinv, node, fring[s][1]);
-    if (own && r >= J0 && r < J1) ld_node<NC>(xs, node, fring[s][2]);
-  };
-  auto prep_old = [&](int s, Old &O) {
-    O.wc = wring[s];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) O.raw[c] = pring[s][c];
-  };
-  // cell row (row of P, row of N): closes ap (row of P), starts an
-  auto cells = [&](int rlow, const auto &P, const auto &Nr, double *ap, double *an) {
-    const uint32_t wcP = P.wc;
-    double inP[NC], rtP[NC], inN[NC], rtN[NC];
-    derive(P.raw, P.wc, inP, rtP);
-    derive(Nr.raw, Nr.wc, inN, rtN);
-    double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
-    ph.cell(inP, rtP, inN, rtN, wcP, i, rlow, c00, c10, c01, c11);
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) {
-      // lane 0 receives its own right-hand corners: it is a halo column whose
-      // q is never used (valid q needs lanes L-1..L+1), so no zero-fill
-      const double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);
-      const double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
-      ap[t] += c00[t] + up10;
-      an[t] = c01[t] + up11;
-    }
-  };
-  // form r_i, z_i, p_i of row r from q_{i-1} (accq, closed) and the F slot
-  auto form = [&](int r, int s, const Old &O, const double *accq, New &Nw) {
-    const uint32_t m = PH::mask(O.wc);
-    double rv[NC], v[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const double q = ((m >> c) & 1u) ? O.raw[c] : accq[c];
-      Nw.dg[c] = fring[s][1][c];
-      rv[c] = fma(-alpha_prev, q, fring[s][0][c]);
-      Nw.z[c] = rv[c] * Nw.dg[c];
-      v[c] = fma(beta, O.raw[c], Nw.z[c]);
-    }
-    if (own && r >= J0 && r < J1) {
-      const int64_t node = (int64_t)r * nxp + i;
-      st_node<NC>(a.y3 + voff, node, rv);
-      st_node<NC>(a.y2 + voff, node, v);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        part[3] += rv[c] * Nw.z[c];
-        part[4] += rv[c] * rv[c];
-      }
-      double X[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) X[c] = fma(alpha_prev, O.raw[c], fring[s][2][c]);
-      st_node<NC>(xs, node, X);
-    }
-    Nw.wc = O.wc;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) Nw.raw[c] = v[c];
-  };
-  auto emit = [&](int r, const New &Nw, const double *accv) {
-    if (!(own && r >= J0 && r < J1)) return;
-    const uint32_t m = PH::mask(Nw.wc);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const double yv = ((m >> c) & 1u) ? Nw.raw[c] : accv[c];
-      part[0] += Nw.raw[c] * yv;
-      part[1] += Nw.z[c] * yv;
-      part[2] += yv * (yv * Nw.dg[c]);
-    }
-  };
-
-  const int jstart = max(J0 - 2, 0);
-  const int rend = min(J1 + 1, ny);
-  Old OA, OB;
-  New NA, NB;
-  double aoA[NOUT], aoB[NOUT], anA[NOUT], anB[NOUT];
-#pragma unroll
-  for (int s = 0; s < D; ++s) {
-    fetch_p(min(jstart + s, rend), s);
-    fetch_f(min(jstart + s, rend), s);
-  }
-  prep_old(0, OA);
-  fetch_p(min(jstart + D, rend), 0);
-#pragma unroll
-  for (int t = 0; t < NOUT; ++t) aoA[t] = 0.0;
-
-  // step r (ring slot s = (r - jstart) % D for p, (r - 1 - jstart) % D for F):
-  // old cells (r-1, r) close q_{i-1}(r-1); form row r-1; new cells (r-2, r-1)
-  // close q_i(r-2), emitted.  On == A: Old row r-1 in OA, row r -> OB, etc.
-  auto step = [&](int r, int sp, int sf, bool newcells, Old &Op, Old &On, double *aop, double *aon,
-                  New &Np, New &Nn, double *anp, double *ann) {
-    prep_old(sp, On);
-    cells(r - 1, Op, On, aop, aon);
-    form(r - 1, sf, Op, aop, Nn);
-    if (newcells) {
-      cells(r - 2, Np, Nn, anp, ann);
-      emit(r - 2, Np, anp);
-    } else {
-#pragma unroll
-      for (int t = 0; t < NOUT; ++t) ann[t] = 0.0;
-    }
-  };
-
-  bool last_in_b = false;  // parity of row rend's Old/New register sets
-  int r = jstart + 1;
-  // first step (no new row below yet), then unrolled steps: both the register
-  // set parity (2) and the ring slots (3) repeat every 6 steps
-  if (r <= rend) {
-    step(r, 1 % D, 0, false, OA, OB, aoA, aoB, NB, NA, anB, anA);
-    fetch_p(min(r + D, rend), 1 % D);
-    fetch_f(min(r - 1 + D, rend), 0);
-    last_in_b = true;
-    ++r;
-  }
-  while (r <= rend) {
-#pragma unroll
-    for (int u = 1; u < 7; ++u) {
-      if (r <= rend) {
-        const int sp = (u + 1) % D, sf = u % D;
-        if (u % 2 == 1) step(r, sp, sf, true, OB, OA, aoB, aoA, NA, NB, anA, anB);
-        else step(r, sp, sf, true, OA, OB, aoA, aoB, NB, NA, anB, anA);
-        last_in_b = (u % 2 == 0);
-        fetch_p(min(r + D, rend), sp);
-        fetch_f(min(r - 1 + D, rend), sf);
-        ++r;
-      }
-    }
-  }
-  // top of the grid: q_{i-1}(ny) is closed (no cells above); form row ny,
-  // close q_i(ny-1) and q_i(ny)
-  auto tail = [&](int sf) {  // sf: compile-time slot after inlining (no local-memory ring)
-    if (last_in_b) {  // Old(ny) in OB, New(ny-1) in NA
-      form(ny, sf, OB, aoB, NB);
-      cells(ny - 1, NA, NB, anA, anB);
-      emit(ny - 1, NA, anA);
-      emit(ny, NB, anB);
-    } else {
-      form(ny, sf, OA, aoA, NA);
-      cells(ny - 1, NB, NA, anB, anA);
-      emit(ny - 1, NB, anB);
-      emit(ny, NA, anA);
-    }
-  };
-  if (rend == ny && jstart < ny) {
-    const int sf = (ny - jstart) % D;
-    if (sf == 0) tail(0);
-    else if (sf == 1) tail(1);
-    else tail(2);
-  }
-}
-
-// The same pass with its prefetch ring in shared memory: every lane copies its
-// own node of each source row (p_{i-1}, r_{i-1}, M^-1, x; 16-byte cp.async,
-// word: the aligned 4-byte chunk that holds it) kRqAhead rows ahead and reads
-// back only what it copied itself, so per-thread cp.async.wait_group orders
-// the ring (no barriers).  Takes ~48 registers of ring out of the register
-// file (more resident warps) and allows a deeper prefetch.
-#ifndef LSG_RQ_AHEAD
-#define LSG_RQ_AHEAD 3
-#endif
-constexpr int kRqAhead = LSG_RQ_AHEAD;
-template <int NC>
+template <int NC, int A>
 struct RqRing {
   static constexpr int FS = 32 * NC;            // doubles per field per slot
   static constexpr int SLOT = 4 * FS + 16;      // p, r, M^-1, x + 32 words
-  static constexpr int D = kRqAhead + 1;        // slots
+  static constexpr int D = A + 1;               // slots
   static constexpr int WARP = D * SLOT;         // doubles per warp
 };
 
@@ -921,13 +719,13 @@ __device__ __forceinline__ void cp_async_wait_all_but() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <class PH>
+template <class PH, int A>
 __device__ __forceinline__ void march_pcg_rqs(const PH &ph, const Geo &g, const MArgs &a, int bx,
                                               int by, int rhs, double beta, double alpha_prev,
                                               double (&part)[5], double *ring) {
   constexpr int NC = PH::NC, NOUT = PH::NOUT;
-  using RG = RqRing<NC>;
-  constexpr int A = kRqAhead, D = RG::D, FS = RG::FS;
+  using RG = RqRing<NC, A>;
+  constexpr int D = RG::D, FS = RG::FS;
   static_assert(PH::NIN == NC, "PCG operators read one field");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int strip = bx * kWarps + warp;
@@ -1125,335 +923,18 @@ __device__ __forceinline__ void march_pcg_rqs(const PH &ph, const Geo &g, const 
   }
 }
 
-template <class PH>
+template <class PH, int A>
 __global__ void __launch_bounds__(kThreads) march_pcg_rqs_kernel(PH ph, Geo g, MArgs a) {
   constexpr int NP = 5;
   __shared__ double scratch[NP * kWarps];
-  __shared__ __align__(16) double ring[kWarps * RqRing<PH::NC>::WARP];
+  __shared__ __align__(16) double ring[kWarps * RqRing<PH::NC, A>::WARP];
   const int rhs = blockIdx.z;
   const lsg_pcg_scalars &s = a.scal[rhs];
   if (s.done != 0.0) return;
   double part[NP];
 #pragma unroll
   for (int t = 0; t < NP; ++t) part[t] = 0.0;
-  march_pcg_rqs<PH>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.beta, s.alpha, part, ring);
-  const int nblk = gridDim.x * gridDim.y;
-  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
-  double tot[NP];
-  const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
-  if (block_partial_and_total<NP, 0u>(part, a.partials + pbase, a.counters + rhs, blk, nblk,
-                                      scratch, tot)) {
-    if (threadIdx.x == 0) pcg_decide(a.scal[rhs], tot);
-  }
-}
-
-// ----------------------------------------------------------------------------
-// Recompute-q pass, software-pipelined ("rqp"): the two stencils of a step are
-// independent dependency chains.  At step r the pass runs
-//   NEW(r-2): new cells (r-3, r-2) on p_i -> closes q_i(r-3), its sums;
-//   OLD(r):   old cells (r-1, r) on p_{i-1} -> closes q_{i-1}(r-1);
-//   FORM(r-1): r_i, z_i, p_i, x_i of row r-1 (stores; p_i also into the ring),
-// so NEW does not wait for this step's FORM and the scheduler can overlap the
-// chains.  Every per-row value lives in a shared-memory ring of D = A + 3 row
-// slots (p_{i-1}, r_{i-1}, M^-1, x fetched by per-lane cp.async A rows ahead;
-// p_i written by FORM); only the two open accumulator rows are registers.
-// z_i.q_i is not summed directly: with p_i = z_i + beta_i p_{i-1} and A
-// symmetric, z_i.q_i = p_i.q_i - beta_i q_{i-1}.p_i, and q_{i-1}.p_i is a
-// row-local sum at FORM time (p_{i-1}.q_i ~ 0 by conjugacy: no cancellation).
-// ----------------------------------------------------------------------------
-#ifndef LSG_RQP_AHEAD
-#define LSG_RQP_AHEAD 2
-#endif
-#ifndef LSG_RQP_WARPS
-#define LSG_RQP_WARPS 2
-#endif
-constexpr int kRqpAhead = LSG_RQP_AHEAD;
-constexpr int kRqpWarps = LSG_RQP_WARPS;
-template <int NC>
-struct RqpRing {
-  static constexpr int FS = 32 * NC;        // doubles per field per slot
-  static constexpr int SLOT = 5 * FS + 16;  // p_{i-1}, r_{i-1}, M^-1, x, p_i + 32 words
-  static constexpr int D = kRqpAhead + 3;
-  static constexpr int WARP = D * SLOT;
-};
-
-template <class PH>
-__device__ __forceinline__ void march_pcg_rqp(const PH &ph, const Geo &g, const MArgs &a, int bx,
-                                              int by, int rhs, double beta, double alpha_prev,
-                                              double (&part)[5], double *ring) {
-  constexpr int NC = PH::NC, NOUT = PH::NOUT;
-  using RG = RqpRing<NC>;
-  constexpr int A = kRqpAhead, D = RG::D, FS = RG::FS;
-  enum { FP = 0, FR = 1, FD = 2, FX = 3, FN = 4 };
-  static_assert(PH::NIN == NC, "PCG operators read one field");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int strip = bx * kRqpWarps + warp;
-  const uint8_t *words = static_cast<const uint8_t *>(a.words);
-  const int nx = g.nx, ny = g.ny;
-  const int64_t nxp = nx + 1;
-  const int64_t nn = nxp * (ny + 1);
-  const int i = strip * kStripRq - 2 + lane;
-  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
-  const bool own = node_ok && lane >= 2 && lane <= kStripRq + 1;
-  const int ic = min(max(i, 0), nx);
-  const int J0 = by * a.seg;
-  const int J1 = min(J0 + a.seg, ny + 1);
-  const size_t voff = (size_t)rhs * (size_t)nn * NC;
-  const double *r_in = a.x + voff, *p_in = a.x2 + voff;
-  double *xs = a.xs + voff;
-  double *myring = ring + (size_t)warp * RG::WARP;
-  const int jstart = max(J0 - 2, 0);
-  const int rend = min(J1 + 1, ny);
-  const int last_formed = (rend == ny) ? rend : rend - 1;
-
-  auto slot = [&](int r) -> int { return (r - jstart) % D; };
-  auto fld = [&](int sl, int f) -> double * { return myring + sl * RG::SLOT + f * FS + lane * NC; };
-  auto cpy = [&](double *dst, const double *src) {
-    if constexpr (NC == 2) cp_async16(dst, src);
-    else cp_async8(dst, src);
-  };
-  auto fetch = [&](int r) {
-    const int rr = min(r, rend);
-    const int sl = slot(r);
-    const int64_t node = (int64_t)rr * nxp + ic;
-    cpy(fld(sl, FP), p_in + node * NC);
-    cpy(fld(sl, FR), r_in + node * NC);
-    cpy(fld(sl, FD), a.dinv + node * NC);
-    if (own && rr >= J0 && rr < J1) cpy(fld(sl, FX), xs + node * NC);
-    uint32_t *W = reinterpret_cast<uint32_t *>(myring + sl * RG::SLOT + 5 * FS);
-    const int64_t wq = node & ~(int64_t)3;
-    if (wq + 4 <= nn) cp_async4(W + lane, words + wq);
-    else W[lane] = (uint32_t)words[node] << (8 * (node & 3));  // the grid's last 1-3 nodes
-    cp_async_commit();
-  };
-  auto ld = [&](int sl, int f, double *v) {
-    const double *S = fld(sl, f);
-    if constexpr (NC == 2) {
-      const double2 t = *reinterpret_cast<const double2 *>(S);
-      v[0] = t.x;
-      v[1] = t.y;
-    } else {
-      v[0] = S[0];
-    }
-  };
-  auto st = [&](int sl, int f, const double *v) {
-    double *S = fld(sl, f);
-    if constexpr (NC == 2) *reinterpret_cast<double2 *>(S) = make_double2(v[0], v[1]);
-    else S[0] = v[0];
-  };
-  auto word = [&](int r, int sl) -> uint32_t {
-    const uint32_t w4 = reinterpret_cast<const uint32_t *>(myring + sl * RG::SLOT + 5 * FS)[lane];
-    const uint32_t sh = 8u * (uint32_t)(((int64_t)r * nxp + ic) & 3);
-    return node_ok ? (w4 >> sh) & 0xffu : 0u;
-  };
-  // cell row (rlow, rlow+1) on field f: closes ap (row rlow), starts an
-  auto cells = [&](int rlow, const double *vP, uint32_t wP, const double *vN, uint32_t wN, double *ap,
-                   double *an) {
-    double inP[NC], rtP[NC], inN[NC], rtN[NC];
-    const uint32_t mP = PH::mask(wP), mN = PH::mask(wN);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      inP[c] = ((mP >> c) & 1u) ? 0.0 : vP[c];
-      inN[c] = ((mN >> c) & 1u) ? 0.0 : vN[c];
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      rtP[c] = __shfl_down_sync(0xffffffffu, inP[c], 1);
-      rtN[c] = __shfl_down_sync(0xffffffffu, inN[c], 1);
-    }
-    double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
-    ph.cell(inP, rtP, inN, rtN, wP, i, rlow, c00, c10, c01, c11);
-#pragma unroll
-    for (int t = 0; t < NOUT; ++t) {
-      const double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);  // lane 0: halo, unused
-      const double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
-      ap[t] += c00[t] + up10;
-      an[t] = c01[t] + up11;
-    }
-  };
-
-  double aoP[NOUT], aoN[NOUT], anP[NOUT], anN[NOUT];
-#pragma unroll
-  for (int t = 0; t < NOUT; ++t) aoP[t] = anP[t] = 0.0;
-
-  // NEW(x): new cells (x-1, x) close q_i(x-1) (accumulator anP) and emit it
-  auto stage_new = [&](int x) {
-    const int s1 = slot(x - 1), s2 = slot(x);
-    double v1[NC], v2[NC], dg[NC];
-    ld(s1, FN, v1);
-    ld(s2, FN, v2);
-    const uint32_t w1 = word(x - 1, s1), w2 = word(x, s2);
-    cells(x - 1, v1, w1, v2, w2, anP, anN);
-    ld(s1, FD, dg);
-    const uint32_t m = PH::mask(w1);
-    if (own && x - 1 >= J0 && x - 1 < J1) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double yv = ((m >> c) & 1u) ? v1[c] : anP[c];
-        part[0] += v1[c] * yv;
-        part[2] += yv * (yv * dg[c]);
-      }
-    }
-  };
-  // OLD(r) + FORM(r-1)
-  auto stage_old_form = [&](int r, bool form) {
-    const int s0 = slot(r - 1), s1 = slot(r);
-    double P0[NC], P1[NC];
-    ld(s0, FP, P0);
-    ld(s1, FP, P1);
-    const uint32_t w0 = word(r - 1, s0), w1 = word(r, s1);
-    cells(r - 1, P0, w0, P1, w1, aoP, aoN);
-    if (!form) return;
-    const uint32_t m = PH::mask(w0);
-    double R[NC], dg[NC], rv[NC], z[NC], v[NC];
-    ld(s0, FR, R);
-    ld(s0, FD, dg);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const double q = ((m >> c) & 1u) ? P0[c] : aoP[c];
-      rv[c] = fma(-alpha_prev, q, R[c]);
-      z[c] = rv[c] * dg[c];
-      v[c] = fma(beta, P0[c], z[c]);
-      aoP[c] = q;  // q_{i-1} of row r-1 (masked), for q_{i-1}.p_i
-    }
-    st(s0, FN, v);
-    const int rf = r - 1;
-    if (own && rf >= J0 && rf < J1) {
-      const int64_t node = (int64_t)rf * nxp + i;
-      st_node<NC>(a.y3 + voff, node, rv);
-      st_node<NC>(a.y2 + voff, node, v);
-      double X[NC];
-      ld(s0, FX, X);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        part[1] += aoP[c] * v[c];
-        part[3] += rv[c] * z[c];
-        part[4] += rv[c] * rv[c];
-        X[c] = fma(alpha_prev, P0[c], X[c]);
-      }
-      st_node<NC>(xs, node, X);
-    }
-  };
-  // FORM(ny) at the top of the grid (q_{i-1}(ny) closed: no cells above)
-  auto stage_form_top = [&]() {
-    const int s0 = slot(ny);
-    double P0[NC];
-    ld(s0, FP, P0);
-    const uint32_t m = PH::mask(word(ny, s0));
-    double R[NC], dg[NC], rv[NC], z[NC], v[NC], q[NC];
-    ld(s0, FR, R);
-    ld(s0, FD, dg);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      q[c] = ((m >> c) & 1u) ? P0[c] : aoP[c];
-      rv[c] = fma(-alpha_prev, q[c], R[c]);
-      z[c] = rv[c] * dg[c];
-      v[c] = fma(beta, P0[c], z[c]);
-    }
-    st(s0, FN, v);
-    if (own && ny >= J0 && ny < J1) {
-      const int64_t node = (int64_t)ny * nxp + i;
-      st_node<NC>(a.y3 + voff, node, rv);
-      st_node<NC>(a.y2 + voff, node, v);
-      double X[NC];
-      ld(s0, FX, X);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        part[1] += q[c] * v[c];
-        part[3] += rv[c] * z[c];
-        part[4] += rv[c] * rv[c];
-        X[c] = fma(alpha_prev, P0[c], X[c]);
-      }
-      st_node<NC>(xs, node, X);
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s <= A; ++s) fetch(jstart + s);
-  for (int r = jstart + 1; r <= rend + 2; ++r) {
-    cp_async_wait_all_but<A - 1>();  // row min(r, rend) has landed
-    if (r >= jstart + 3 && r <= rend) {  // steady state: both chains, one block
-      stage_new(r - 2);
-      stage_old_form(r, true);
-#pragma unroll
-      for (int t = 0; t < NOUT; ++t) {
-        anP[t] = anN[t];
-        aoP[t] = aoN[t];
-      }
-    } else {
-      if (r - 2 >= jstart + 1 && r - 2 <= last_formed) {
-        stage_new(r - 2);
-#pragma unroll
-        for (int t = 0; t < NOUT; ++t) anP[t] = anN[t];
-        if (r - 2 == ny) {  // q_i(ny) is closed too
-          const int sl = slot(ny);
-          double v1[NC], dg[NC];
-          ld(sl, FN, v1);
-          ld(sl, FD, dg);
-          const uint32_t m = PH::mask(word(ny, sl));
-          if (own && ny >= J0 && ny < J1) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              const double yv = ((m >> c) & 1u) ? v1[c] : anP[c];
-              part[0] += v1[c] * yv;
-              part[2] += yv * (yv * dg[c]);
-            }
-          }
-        }
-      }
-      if (r <= rend) {
-        stage_old_form(r, true);
-#pragma unroll
-        for (int t = 0; t < NOUT; ++t) aoP[t] = aoN[t];
-      } else if (r - 1 == rend && rend == ny) {
-        stage_form_top();
-      }
-    }
-    fetch(r + A);  // into the slot of row r-3, read for the last time above
-  }
-  cp_async_wait_all_but<0>();
-}
-
-template <class PH>
-__global__ void __launch_bounds__(kRqpWarps * 32) march_pcg_rqp_kernel(PH ph, Geo g, MArgs a) {
-  constexpr int NP = 5;
-  __shared__ double scratch[NP * kRqpWarps];
-  extern __shared__ __align__(16) double rqp_ring[];
-  const int rhs = blockIdx.z;
-  const lsg_pcg_scalars &s = a.scal[rhs];
-  if (s.done != 0.0) return;
-  const double beta = s.beta;
-  double part[NP];
-#pragma unroll
-  for (int t = 0; t < NP; ++t) part[t] = 0.0;
-  march_pcg_rqp<PH>(ph, g, a, blockIdx.x, blockIdx.y, rhs, beta, s.alpha, part, rqp_ring);
-  const int nblk = gridDim.x * gridDim.y;
-  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
-  double tot[NP];
-  const size_t pbase = (size_t)rhs * (size_t)nblk * NP;
-  if (block_partial_and_total<NP, 0u>(part, a.partials + pbase, a.counters + rhs, blk, nblk,
-                                      scratch, tot)) {
-    if (threadIdx.x == 0) {
-      tot[1] = tot[0] - beta * tot[1];  // z.q = p.q - beta q_{i-1}.p
-      pcg_decide(a.scal[rhs], tot);
-    }
-  }
-}
-
-#ifndef LSG_M2_RQ_MINB
-#define LSG_M2_RQ_MINB 3
-#endif
-template <class PH>
-__global__ void __launch_bounds__(kThreads, LSG_M2_RQ_MINB) march_pcg_rq_kernel(PH ph, Geo g, MArgs a) {
-  constexpr int NP = 5;
-  __shared__ double scratch[NP * kWarps];
-  const int rhs = blockIdx.z;
-  const lsg_pcg_scalars &s = a.scal[rhs];
-  if (s.done != 0.0) return;
-  double part[NP];
-#pragma unroll
-  for (int t = 0; t < NP; ++t) part[t] = 0.0;
-  march_pcg_rq<PH>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.beta, s.alpha, part);
+  march_pcg_rqs<PH, A>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.beta, s.alpha, part, ring);
   const int nblk = gridDim.x * gridDim.y;
   const int blk = blockIdx.y * gridDim.x + blockIdx.x;
   double tot[NP];

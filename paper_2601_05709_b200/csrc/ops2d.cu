@@ -223,8 +223,8 @@ static int nstrips_of(const Geo &g) { return (int)ceil_div(g.nx + 1, kStrip); }
 constexpr int kSMs = 148;
 constexpr int kMaxPartials = 4096;  // >= CTAs per rhs of any launch below
 
-static int seg_for(const Geo &g, int k, int ctas_per_sm, int nstrips = -1, int warps = kWarps) {
-  const int64_t cols = ceil_div(nstrips < 0 ? nstrips_of(g) : nstrips, warps);
+static int seg_for(const Geo &g, int k, int ctas_per_sm, int nstrips = -1) {
+  const int64_t cols = ceil_div(nstrips < 0 ? nstrips_of(g) : nstrips, kWarps);
   const int64_t rows = g.ny + 1;
   int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 4);
   int64_t nseg = slots / (cols * k);
@@ -304,29 +304,25 @@ static int launch_march(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t
   return check_launch("march2d");
 }
 
-// The recompute-q PCG pass: 28-column strips, its own occupancy-sized grid.
-// LSG_PCG2D_RQ: 0 = stored-q pass (march_pcg), 1 = recompute pass with a
-// register prefetch ring (march_pcg_rq), 2 = with the shared-memory cp.async
-// ring (march_pcg_rqs, default), 3 = software-pipelined with the whole row state in a
-// shared-memory ring (march_pcg_rqp).
-static int pcg_rq_mode() {
+// The recompute-q PCG pass (march_pcg_rqs): 28-column strips, its own
+// occupancy-sized grid.  LSG_PCG2D_RQ=0 keeps the stored-q pass (march_pcg);
+// LSG_RQ_AHEAD=2|3 overrides the prefetch depth.
+static bool pcg_rq_on() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("LSG_PCG2D_RQ");
-    v = e ? atoi(e) : 2;
-    if (v < 0 || v > 3) v = 3;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
-  return v;
+  return v == 1;
 }
 
-template <class PH, bool SMEM>
+template <class PH, int A>
 static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   static int ctas_per_sm = -1;
   if (ctas_per_sm < 0) {
-    const cudaError_t e0 =
-        SMEM ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH>, kThreads, 0)
-             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rq_kernel<PH>, kThreads, 0);
-    if (e0 != cudaSuccess) ctas_per_sm = 3;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH, A>,
+                                                      kThreads, 0) != cudaSuccess)
+      ctas_per_sm = 4;
     const char *e = getenv("LSG_M2_GRID_CTAS");
     if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
   }
@@ -334,48 +330,29 @@ static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_
   a.seg = seg_for(g, k, ctas_per_sm, a.nstrips);
   const dim3 grid((unsigned)ceil_div(a.nstrips, kWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
                   (unsigned)k);
-  if (SMEM) march_pcg_rqs_kernel<PH><<<grid, kThreads, 0, st>>>(ph, g, a);
-  else march_pcg_rq_kernel<PH><<<grid, kThreads, 0, st>>>(ph, g, a);
+  march_pcg_rqs_kernel<PH, A><<<grid, kThreads, 0, st>>>(ph, g, a);
   return check_launch("march2d_pcg_rq");
 }
 
 template <class PH>
-static int launch_pcg_rqp(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
-  constexpr int threads = kRqpWarps * 32;
-  const size_t smem = sizeof(double) * kRqpWarps * RqpRing<PH::NC>::WARP;
-  static int ctas_per_sm = -1;
-  if (ctas_per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqp_kernel<PH>, threads,
-                                                      smem) != cudaSuccess)
-      ctas_per_sm = 8;
-    const char *e = getenv("LSG_M2_GRID_CTAS");
-    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
+static int launch_pcg_rq_depth(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char *e = getenv("LSG_RQ_AHEAD");
+    forced = e ? atoi(e) : 0;
   }
-  a.nstrips = (int)ceil_div(g.nx + 1, kStripRq);
-  a.seg = seg_for(g, k, ctas_per_sm, a.nstrips, kRqpWarps);
-  const dim3 grid((unsigned)ceil_div(a.nstrips, kRqpWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
-                  (unsigned)k);
-  march_pcg_rqp_kernel<PH><<<grid, threads, smem, st>>>(ph, g, a);
-  return check_launch("march2d_pcg_rqp");
+  // measured: 3 rows ahead pays only on small batched grids (cfg2 1024x256 k=8:
+  // 51.6 vs 52.5 us); 2 elsewhere (4096x2048 k=1: 183 vs 198; 2048x1024 k=2: 94 vs 98)
+  const int64_t nn = (int64_t)(g.nx + 1) * (g.ny + 1);
+  const int depth = (forced == 2 || forced == 3) ? forced : (k > 1 && nn < (1 << 20) ? 3 : 2);
+  return depth == 3 ? launch_pcg_rq<PH, 3>(ph, g, a, k, st) : launch_pcg_rq<PH, 2>(ph, g, a, k, st);
 }
 
 static int dispatch_pcg_rq(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
-  if (pcg_rq_mode() == 3) {
-    if (op.kind == LSG_OP_ELASTICITY) return launch_pcg_rqp<Elast>(make_elast(g, op), g, a, k, st);
-    if (op.kind == LSG_OP_H1) return launch_pcg_rqp<H1>(make_h1(g, op), g, a, k, st);
-    if (op.kind == LSG_OP_LAPLACE) return launch_pcg_rqp<Lap>(make_lap(g, op), g, a, k, st);
-  }
-  const bool sm = pcg_rq_mode() == 2;
-  if (op.kind == LSG_OP_ELASTICITY)
-    return sm ? launch_pcg_rq<Elast, true>(make_elast(g, op), g, a, k, st)
-              : launch_pcg_rq<Elast, false>(make_elast(g, op), g, a, k, st);
-  if (op.kind == LSG_OP_H1)
-    return sm ? launch_pcg_rq<H1, true>(make_h1(g, op), g, a, k, st)
-              : launch_pcg_rq<H1, false>(make_h1(g, op), g, a, k, st);
-  if (op.kind == LSG_OP_LAPLACE)
-    return sm ? launch_pcg_rq<Lap, true>(make_lap(g, op), g, a, k, st)
-              : launch_pcg_rq<Lap, false>(make_lap(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_ELASTICITY) return launch_pcg_rq_depth<Elast>(make_elast(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_H1) return launch_pcg_rq_depth<H1>(make_h1(g, op), g, a, k, st);
+  if (op.kind == LSG_OP_LAPLACE) return launch_pcg_rq_depth<Lap>(make_lap(g, op), g, a, k, st);
   set_error("unknown operator kind %d", op.kind);
   return LSG_ERR_ARG;
 }
@@ -656,7 +633,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     a.y3 = odd ? ws.r : ws.r_alt;  // ... and of this one
     a.y2 = odd ? ws.p : ws.p_alt;
     a.y = odd ? ws.q : ws.q_alt;
-    int rc = pcg_rq_mode() ? dispatch_pcg_rq(op, a, ws.k, st) : dispatch_op<PCG>(op, a, ws.k, st);
+    int rc = pcg_rq_on() ? dispatch_pcg_rq(op, a, ws.k, st) : dispatch_op<PCG>(op, a, ws.k, st);
     if (rc) return rc;
     ws.parity ^= 1;
   }

@@ -99,11 +99,13 @@ print("ok")
 def test_shape_sweep_graph_paths(tmp_path):
     """The 2D grid-shape sweep (state PCG, velocity CG) with the persistent
     kernel off, so every solve runs the per-launch single pass: the default
-    recompute-q pass (28-column strips, two halo rows per segment) and the
-    stored-q pass, on grids around every tile edge and with many row segments."""
+    recompute-q pass (28-column strips, two halo rows per segment) at both
+    prefetch depths and the stored-q pass, on grids around every tile edge and with many row segments."""
     script = tmp_path / "sweep.py"
     script.write_text(SWEEP % {"root": ROOT, "tests": os.path.join(ROOT, "tests")})
-    for env in ({"LSG_PCG2D_PERSISTENT": "0"}, {"LSG_PCG2D_PERSISTENT": "0", "LSG_PCG2D_RQ": "0"}):
+    for env in ({"LSG_PCG2D_PERSISTENT": "0"}, {"LSG_PCG2D_PERSISTENT": "0", "LSG_RQ_AHEAD": "2"},
+                {"LSG_PCG2D_PERSISTENT": "0", "LSG_RQ_AHEAD": "3"},
+                {"LSG_PCG2D_PERSISTENT": "0", "LSG_PCG2D_RQ": "0"}):
         res = subprocess.run([sys.executable, str(script)], env=dict(os.environ, **env),
                              capture_output=True, text=True, timeout=900)
         assert res.returncode == 0 and res.stdout.strip().endswith("ok"), (env, res.stderr[-3000:])
