@@ -60,7 +60,7 @@ def parse():
 def ncu_traffic():
     """DRAM bytes per fused PCG iteration from the committed ncu --set full capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_pcg.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_pcg_rq.json")) as f:
             return float(json.load(f)["traffic_bytes_per_pcg_iteration"])
     except Exception:
         return None
@@ -348,16 +348,18 @@ def b200_arm(args, world, rank, local):
                              "standalone apply timings flush L2 with a 256 MB write",
                        "parallelism": (f"load cases sharded over {world} GPUs" if sharded else
                                        f"replicas x{world}" if world > 1 else "single GPU")},
-            "roofline": {"bound": "hbm", "kernel": "fused PCG iteration (pass A: p-update + "
-                                                   "elasticity apply + p.q ; pass B: x/r update + "
-                                                   "Jacobi + r.z, r.r)",
+            "roofline": {"bound": "hbm", "kernel": "single-pass PCG iteration march_pcg_rqs "
+                                                   "(r, z, p, x of iteration i and q_i = A p_i in one "
+                                                   "launch; q_{i-1} = A p_{i-1} recomputed, not stored)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(),
-                         "traffic_note": "DRAM bytes of one PCG iteration, pass A + pass B, from "
-                                         "profiles/r01_ncu_pcg.json (cold cache); below the "
-                                         "algorithmic count because x += alpha p is folded into "
-                                         "pass A (9 of the canonical 10 vectors) and some writes "
-                                         "stay in L2",
+                         "traffic_note": "DRAM bytes of one PCG iteration (one launch) from "
+                                         "profiles/r01_ncu_pcg_rq.json (cold cache): below the "
+                                         "algorithmic (canonical two-pass, 10 vectors per rhs) "
+                                         "count because the pass moves 6 vectors per rhs (q is "
+                                         "recomputed, x updated in the same pass) and some writes "
+                                         "stay in L2; achieved/peak is the canonical-byte rate, the "
+                                         "actual DRAM rate is traffic / launch time",
                          "peak_kind": peak_kind,
                          "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration",
                          "pcg_ms_in_timed_region": pcg_ms, "pcg_share_of_step": all_ms / (t_local * 1e3),

@@ -187,8 +187,9 @@ int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream);
  * scipy.sparse.linalg.cg): stop when ||r|| < max(atol, rtol*||b||), checked
  * before each iteration; b == 0 returns x = b.  x holds the warm start on
  * entry.  lsg_pcg_start computes r = b - A x and the stopping thresholds;
- * lsg_pcg_iterate enqueues `niter` more iterations (two fused kernels each);
- * converged right-hand sides freeze.  Poll ws->scal (done, iters). */
+ * lsg_pcg_iterate enqueues `niter` more iterations (2D: one kernel each,
+ * 3D: three); converged right-hand sides freeze.  Poll ws->scal (done, iters).
+ * 2D: lsg_pcg_start zeroes ws->p (the first pass reads it as p_{-1}). */
 int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol,
                   double maxiter, void *stream);
 int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream);
@@ -198,13 +199,12 @@ int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *strea
  * launches the chunk kernels directly instead. */
 void lsg_graph_stats(double *out4);
 
-/* The updates x += alpha p are folded into pass A, which reads p anyway: in
- * 2D that of iteration i into pass A of i+1; in 3D those of iterations i-2
- * and i-1 into the elementwise half of pass A of every even iteration i
- * (directions rotate through p, p_alt, p_ring), which halves the x traffic.
- * A right-hand side that has just converged therefore has one or two updates
- * pending: call lsg_pcg_finish once after the last lsg_pcg_iterate, before
- * reading x. */
+/* 2D: the single pass of iteration i forms x_i together with r_i, so nothing
+ * is pending.  3D: the updates x += alpha p of iterations i-2 and i-1 are
+ * folded into the elementwise pass of every even iteration i (directions
+ * rotate through p, p_alt, p_ring), which halves the x traffic; a right-hand
+ * side that has just converged has one or two updates pending.  Call
+ * lsg_pcg_finish once after the last lsg_pcg_iterate, before reading x. */
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream);
 
 /* Fused compliance evaluation + shape-derivative right-hand side --
