@@ -719,7 +719,9 @@ __device__ __forceinline__ void march_pcg(const PH &ph, const Geo &g, const MArg
 // on large ones (cfg4: 183 vs 198 us).  (Also measured and removed: the register ring,
 // 52.9 / 185 us; a software-pipelined variant whose two stencils overlap as
 // independent chains with all row state in the ring, 57.3 / 204 us; keeping
-// the masked inputs in registers, 79 / 254 us.)
+// the masked inputs in registers, 79 / 254 us; two right-hand sides per warp
+// sharing words, weights, masks and M^-1 (168 registers, 3 CTAs/SM), 54.7 vs
+// 49.5 us on the same box; strength-reduced ring/row addressing, no change.)
 // ----------------------------------------------------------------------------
 constexpr int kStripRq = 28;
 
