@@ -1047,39 +1047,111 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
   return check_launch("zero_if_flag3d");
 }
 
-int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
-  const int64_t n = 3 * nodes_of(geo_of(op.grid));
+// One 3D PCG iteration (elementwise p-pass, stencil q = A p, update) of a
+// batch of right-hand sides; `after_prep` is recorded once the p-pass is queued.
+static int iterate_once(const lsg_op &op, const lsg_pcg_ws &ws, int parity, int64_t n, dim3 eg,
+                        cudaStream_t st, cudaEvent_t after_prep) {
   MArgs a = {};
   a.y = ws.q;
   a.dinv = ws.dinv;
   a.scal = ws.scal;
   a.partials = ws.partials;
   a.counters = ws.counters;
+  double *const ring[3] = {ws.p, ws.p_alt, ws.p_ring};
+  const int ph = parity;  // iteration index mod 3 = slot of the new direction
+  double *p_new = ring[ph], *p_old = ring[ph == 0 ? 2 : ph - 1];
+  double *p_old2 = ring[ph == 2 ? 0 : ph + 1];
+  pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_old2, p_new, ws.x, ws.scal);
+  int rc = check_launch("pcg_prep3d");
+  if (rc) return rc;
+  if (after_prep && cudaEventRecord(after_prep, st) != cudaSuccess) return check_launch("event");
+  a.x = p_new;
+  rc = dispatch<PCGQ>(op, a, ws.k, st);
+  if (rc) return rc;
+  pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
+  return check_launch("pcg_update3d");
+}
+
+// The right-hand sides of one batch starting at r0 (pointer offsets only).
+static lsg_pcg_ws sub_ws(const lsg_pcg_ws &ws, int r0, int k, int64_t n) {
+  lsg_pcg_ws g = ws;
+  const size_t off = (size_t)r0 * (size_t)n;
+  g.k = k;
+  g.x = ws.x + off;
+  g.b = ws.b + off;
+  g.r = ws.r + off;
+  g.p = ws.p + off;
+  g.q = ws.q + off;
+  g.p_alt = ws.p_alt + off;
+  g.p_ring = ws.p_ring + off;
+  g.scal = ws.scal + r0;
+  g.partials = ws.partials + (size_t)r0 * kMaxPartials * 8;
+  g.counters = ws.counters + r0;
+  return g;
+}
+
+// A batch of k >= 2 right-hand sides runs as two halves on two streams, the
+// second half's iteration starting once the first half's p-pass is done, so
+// that one half's HBM-bound elementwise passes can run beside the other
+// half's fp64-bound stencil (cfg5: 471 -> 461 us per iteration; the stencil
+// still takes every free SM, so the overlap is partial).  LSG_PCG3D_STREAMS=1
+// keeps one stream.
+static int streams3d() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_PCG3D_STREAMS");
+    v = e ? atoi(e) : 2;
+    if (v != 2) v = 1;
+  }
+  return v;
+}
+
+int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
+  const int64_t n = 3 * nodes_of(geo_of(op.grid));
   static int ew = -1;  // LSG_EW_CTAS: elementwise CTAs per SM (experiments)
   if (ew < 0) {
     const char *e = getenv("LSG_EW_CTAS");
     ew = e ? atoi(e) : 4;
     if (ew < 1) ew = 1;
   }
-  int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
-  int64_t slots = (int64_t)kSMs * ew / ws.k;
-  if (slots < 1) slots = 1;
-  const dim3 eg((unsigned)(need < slots ? need : slots), (unsigned)ws.k);
-  double *const ring[3] = {ws.p, ws.p_alt, ws.p_ring};
+  auto grid_for = [&](int k) {
+    int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
+    int64_t slots = (int64_t)kSMs * ew / k;
+    if (slots < 1) slots = 1;
+    return dim3((unsigned)(need < slots ? need : slots), (unsigned)k);
+  };
+  if (streams3d() == 2 && ws.k >= 2) {
+    static cudaStream_t st2 = nullptr;
+    static cudaEvent_t ev_fork = nullptr, ev_prep = nullptr, ev_join = nullptr;
+    if (!st2) {
+      if (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_prep, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return check_launch("pcg3d streams");
+    }
+    const int k1 = ws.k / 2, k2 = ws.k - k1;
+    const lsg_pcg_ws w1 = sub_ws(ws, 0, k1, n), w2 = sub_ws(ws, k1, k2, n);
+    const dim3 g1 = grid_for(k1), g2 = grid_for(k2);
+    if (cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(st2, ev_fork, 0) != cudaSuccess)
+      return check_launch("pcg3d fork");
+    for (int it = 0; it < niter; ++it) {
+      int rc = iterate_once(op, w1, ws.parity, n, g1, st, ev_prep);
+      if (rc) return rc;
+      if (cudaStreamWaitEvent(st2, ev_prep, 0) != cudaSuccess) return check_launch("pcg3d wait");
+      rc = iterate_once(op, w2, ws.parity, n, g2, st2, nullptr);
+      if (rc) return rc;
+      ws.parity = ws.parity == 2 ? 0 : ws.parity + 1;
+    }
+    if (cudaEventRecord(ev_join, st2) != cudaSuccess || cudaStreamWaitEvent(st, ev_join, 0) != cudaSuccess)
+      return check_launch("pcg3d join");
+    return LSG_OK;
+  }
+  const dim3 eg = grid_for(ws.k);
   for (int it = 0; it < niter; ++it) {
-    const int ph = ws.parity;  // iteration index mod 3 = slot of the new direction
-    double *p_new = ring[ph], *p_old = ring[ph == 0 ? 2 : ph - 1];
-    double *p_old2 = ring[ph == 2 ? 0 : ph + 1];
-    pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_old2, p_new, ws.x, ws.scal);
-    int rc = check_launch("pcg_prep3d");
+    int rc = iterate_once(op, ws, ws.parity, n, eg, st, nullptr);
     if (rc) return rc;
-    a.x = p_new;
-    rc = dispatch<PCGQ>(op, a, ws.k, st);
-    if (rc) return rc;
-    pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
-    rc = check_launch("pcg_update3d");
-    if (rc) return rc;
-    ws.parity = ph == 2 ? 0 : ph + 1;
+    ws.parity = ws.parity == 2 ? 0 : ws.parity + 1;
   }
   return LSG_OK;
 }

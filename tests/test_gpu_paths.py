@@ -109,3 +109,42 @@ def test_shape_sweep_graph_paths(tmp_path):
         res = subprocess.run([sys.executable, str(script)], env=dict(os.environ, **env),
                              capture_output=True, text=True, timeout=900)
         assert res.returncode == 0 and res.stdout.strip().endswith("ok"), (env, res.stderr[-3000:])
+
+
+SCRIPT3D = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, %(root)r)
+from paper_2601_05709_b200 import DirichletSet, ElasticityOperator, FunctionSpace, build_box_mesh
+from paper_2601_05709_b200.fem import solve_batched
+mesh = build_box_mesh((0.0, 0.0, 0.0, 2.0, 1.0, 1.0), (12, 6, 6), [(1, lambda p: p[:, 0] < 1e-12)])
+space = FunctionSpace(mesh, 3)
+rng = np.random.default_rng(5)
+phi = torch.as_tensor(rng.standard_normal(mesh.num_vertices) - 0.2, device="cuda")
+bc = DirichletSet.on_tags(space, 1)
+op = ElasticityOperator(space, phi, (0.576923, 0.384615), 1e-3, bc)
+b = rng.standard_normal((5, space.dof_count)) * np.array([[1.0], [1e-2], [1e3], [0.0], [1.0]])
+b[:, bc.dofs] = 0.0
+x, it = solve_batched(op, torch.as_tensor(b, device="cuda"), rtol=1e-10)
+np.save(sys.argv[1], x.cpu().numpy())
+print(json.dumps([int(v) for v in it.cpu()]))
+"""
+
+
+def test_pcg3d_two_streams_agree(tmp_path):
+    """3D batched PCG split over two streams (default) vs one stream: an odd
+    batch with a zero right-hand side and right-hand sides that converge at
+    different iterations gives the same solutions."""
+    script = tmp_path / "solve3d.py"
+    script.write_text(SCRIPT3D % {"root": ROOT})
+    out = {}
+    for name, env in (("two", {}), ("one", {"LSG_PCG3D_STREAMS": "1"})):
+        res = subprocess.run([sys.executable, str(script), str(tmp_path / f"{name}.npy")],
+                             env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[name] = (np.load(tmp_path / f"{name}.npy"), json.loads(res.stdout.strip().splitlines()[-1]))
+    (x2, it2), (x1, it1) = out["two"], out["one"]
+    assert it2[3] == it1[3] == 0 and not x2[3].any()
+    for r in (0, 1, 2, 4):
+        assert it1[r] > 10 and abs(it1[r] - it2[r]) <= max(2, it1[r] // 50)
+        assert np.linalg.norm(x2[r] - x1[r]) <= 1e-8 * np.linalg.norm(x1[r])
