@@ -115,10 +115,13 @@ typedef struct {
  *   dinv          : n doubles, lsg_inv_diag of the operator (shared by all k)
  * 2D runs one fused pass per iteration: it forms r_i = r_{i-1} - alpha q_{i-1},
  * z = M^-1 r_i, p_i = z + beta p_{i-1}, x += alpha p_{i-1} and q_i = A p_i with
- * neighbouring CTAs recomputing r_i and p_i in their halo, so r, p and q are
- * double-buffered (r/r_alt, p/p_alt, q/q_alt).  3D runs an elementwise pass
- * that forms p, the stencil pass, and an update pass, with three direction
- * buffers (p, p_alt, p_ring).  `parity` (which buffers are current) is owned
+ * neighbouring CTAs recomputing r_i and p_i in their halo, so r and p are
+ * double-buffered (r/r_alt, p/p_alt).  The default pass recomputes
+ * q_{i-1} = A p_{i-1} instead of reading it; q/q_alt are used by the small-
+ * system persistent kernel and the stored-q variant.  3D runs an elementwise
+ * pass that forms p, the stencil pass, and an update pass, with three
+ * direction buffers (p, p_alt, p_ring); a batch of k >= 2 runs as two halves
+ * on two library-owned streams joined back into the caller's stream.  `parity` (which buffers are current) is owned
  * by the library: lsg_pcg_start resets it, lsg_pcg_iterate advances it once
  * per iteration. */
 typedef struct {
