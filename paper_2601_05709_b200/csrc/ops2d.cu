@@ -568,8 +568,13 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
   a.nstrips = nstrips_of(g);
   const dim3 mg = march_grid(g, a.seg, ws.k);
   const int ntask = (int)(mg.x * mg.y * ws.k);
-  // one task per CTA where possible, at least one CTA per SM for the loads
-  int ncta = ntask < kSMs ? kSMs : ntask;
+  // one task per CTA where possible; LSG_PERSIST_FILL=1: at least one CTA per SM
+  static int fill = -1;
+  if (fill < 0) {
+    const char *e = getenv("LSG_PERSIST_FILL");
+    fill = e ? atoi(e) : 1;
+  }
+  int ncta = (fill && ntask < kSMs) ? kSMs : ntask;
   if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
   int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
   double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
