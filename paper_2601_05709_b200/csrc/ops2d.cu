@@ -565,14 +565,27 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
                                                     kThreads, 0) != cudaSuccess)
     ctas_march = 4;
   a.seg = seg_for(g, ws.k, ctas_march);
+  {
+    // LSG_PERSIST_SEGMIN: minimum rows per task (experiments; cfg1: 4 rows 7.0 us,
+    // 8 rows 8.6, 16 rows 11.7 -- the per-iteration barrier and reductions are
+    // cheaper than the longer march)
+    static int segmin = -1;
+    if (segmin < 0) {
+      const char *e = getenv("LSG_PERSIST_SEGMIN");
+      segmin = e ? atoi(e) : 0;
+    }
+    if (a.seg < segmin) a.seg = segmin;
+  }
   a.nstrips = nstrips_of(g);
   const dim3 mg = march_grid(g, a.seg, ws.k);
   const int ntask = (int)(mg.x * mg.y * ws.k);
-  // one task per CTA where possible; LSG_PERSIST_FILL=1: at least one CTA per SM
+  // one task per CTA (cfg1 PCG iteration 7.9 -> 7.0 us against filling every SM:
+  // fewer partials to reduce and CTAs to barrier); LSG_PERSIST_FILL=1: at
+  // least one CTA per SM
   static int fill = -1;
   if (fill < 0) {
     const char *e = getenv("LSG_PERSIST_FILL");
-    fill = e ? atoi(e) : 1;
+    fill = e ? atoi(e) : 0;
   }
   int ncta = (fill && ntask < kSMs) ? kSMs : ntask;
   if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
