@@ -183,8 +183,17 @@ def cpu_sample(c, cg_iters_per_load, threads):
     t0 = time.perf_counter()
     _, nsub = olevel.transport(grid, phi, theta, 1e-3, 8, False, h)
     t_tr = time.perf_counter() - t0
+    # the reference's apply: its assembled, eliminated CSR operator times the k fields
+    A = systems[0][0]
+    U = np.random.default_rng(0).standard_normal((A.shape[0], len(systems)))
+    A @ U
+    t0 = time.perf_counter()
+    for _ in range(5):
+        A @ U
+    t_apply = (time.perf_counter() - t0) / 5
     return {"asm": t_asm, "cg": t_cg, "cg_rhs_iters": cg_iters_per_load * len(systems),
-            "s1": t_s1, "transport": t_tr, "k": len(systems), "n": model.space.dof_count}
+            "s1": t_s1, "transport": t_tr, "k": len(systems), "n": model.space.dof_count,
+            "apply": t_apply}
 
 
 def cpu_iters_per_sec(s, rhs_iters_per_outer):
@@ -337,6 +346,9 @@ def b200_arm(args, world, rank, local):
         s = cpu_sample(c, cg_iters_per_load=25, threads=1)
         v, t_outer = cpu_iters_per_sec(s, rhs_per_outer)
         cpu = {"value": v, "unit": "iters/s", "cores": 1, "kind": "port",
+               "apply_dof_per_s": s["k"] * s["n"] / s["apply"],
+               "apply_note": "scipy CSR (the reference's assembled, Dirichlet-eliminated operator) "
+                             "times the k load-case fields, 1 thread; assembly not included",
                "sample": f"oracle (numpy/scipy restatement of the reference path) on {args.config}: "
                          f"assembly+elimination, 25 scipy-cg Jacobi-PCG iterations x {s['k']} loads, "
                          f"S1 + derivative vector, one transport; extrapolated to "
