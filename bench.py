@@ -303,7 +303,6 @@ def b200_arm(args, world, rank, local):
     t_apply = apply_times(True)
     del flush, clean
     apply_bytes = 16.0 * d * k * N + E
-    del flush
 
     # ---- end to end through the public API from host buffers ----------------------------
     e2e = None

@@ -9,14 +9,6 @@ namespace d2 {
 
 enum Act { APPLY = 0, RESID = 1, PCG = 2, STATS = 3, SHAPE = 4 };
 
-// Rows the 2D apply prefetches ahead.  Measured (L2 flushed, cfg2 / cfg4):
-// 2 rows 24.6 / 69.5 us, 4 rows 22.7 / 73.7, 6 rows 24.6 / 80.9, 8 rows
-// 26.7 / 96.3 -- deeper rings cost registers (66 -> 80+) and resident CTAs.
-#ifndef LSG_APPLY_DEPTH
-#define LSG_APPLY_DEPTH 2
-#endif
-constexpr int kApplyDepth = LSG_APPLY_DEPTH;
-
 #ifndef LSG_M2_PCG_MINB
 #define LSG_M2_PCG_MINB 1  // resident CTAs per SM the PCG pass is register-capped for
 #endif
@@ -488,15 +480,15 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
   const int rend = min(J1, ny);
   Row SA, SB;
   double accA[NOUT], accB[NOUT];
-  // prefetch ring of PD rows: step r consumes slot (r - jstart - 1) % PD and
-  // refills it with row r + PD
-  constexpr int PD = (ACT == APPLY) ? kApplyDepth : 2;
-  Raw ring[PD];
+  // two rows in flight (deeper prefetch rings measured slower for the apply:
+  // cfg2 / cfg4 with L2 flushed, 2 rows 24.6 / 69.5 us, 4 rows 22.7 / 73.7,
+  // 6 rows 24.6 / 80.9, 8 rows 26.7 / 96.3 -- registers 66 -> 80+, fewer CTAs)
+  Raw fA, fB;
   {
     Raw f0;
     fetch(jstart, f0);
-#pragma unroll
-    for (int s = 0; s < PD; ++s) fetch(min(jstart + 1 + s, rend), ring[s]);
+    fetch(min(jstart + 1, rend), fA);
+    fetch(min(jstart + 2, rend), fB);
     prepare(jstart, f0, SA);
   }
 #pragma unroll
@@ -504,19 +496,13 @@ __device__ __forceinline__ void march_core(const PH &ph, const Geo &g, const MAr
 
   bool last_in_b = false;  // which register set holds row rend after the loop
   int r = jstart + 1;
-  constexpr int U = (PD % 2 == 0) ? PD : 2 * PD;  // register-set parity and ring slot repeat
   while (r <= rend) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (r <= rend) {
-        const int s = u % PD;
-        if (u % 2 == 0) step(r, ring[s], SA, SB, accA, accB);
-        else step(r, ring[s], SB, SA, accB, accA);
-        last_in_b = (u % 2 == 0);
-        fetch(min(r + PD, rend), ring[s]);
-        ++r;
-      }
-    }
+    step(r, fA, SA, SB, accA, accB);
+    fetch(min(r + 2, rend), fA);
+    if (++r > rend) { last_in_b = true; break; }
+    step(r, fB, SB, SA, accB, accA);
+    fetch(min(r + 2, rend), fB);
+    ++r;
   }
   if (J1 == ny + 1 && own && ny >= J0) {
     if (last_in_b) emit(ny, SB, accB);
