@@ -30,6 +30,15 @@ int check_launch(const char *what) {
   return LSG_OK;
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int check_grid(const lsg_grid *g) {
   if (!g) { set_error("null grid"); return LSG_ERR_ARG; }
   if (g->dim != 2 && g->dim != 3) { set_error("grid dim must be 2 or 3, got %d", g->dim); return LSG_ERR_ARG; }

@@ -20,6 +20,32 @@ int check_launch(const char *what);
 
 constexpr int kWarp = 32;
 
+// Programmatic dependent launch (PDL) for the PCG-iteration kernels: a kernel
+// launched with launch_pdl may have its CTAs scheduled while its predecessor
+// on the stream is still draining (hiding the launch and CTA-rasterisation
+// latency of the kernel boundary); it calls pdl_wait() before it reads
+// anything its predecessor wrote, which returns once that grid has completed
+// and its memory is visible.  The predecessor triggers implicitly at exit, so
+// a waiting CTA never holds an SM a predecessor CTA still needs.  Outside a
+// programmatic dependency pdl_wait() is a no-op.  LSG_NO_PDL=1 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Asynchronous global -> shared copies (LDGSTS): staged prefetch that costs no
 // registers; .cg (16 bytes) bypasses L1, so it is coherent with data written
 // earlier in the same launch across a grid barrier.

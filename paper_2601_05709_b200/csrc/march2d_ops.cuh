@@ -936,6 +936,7 @@ __global__ void __launch_bounds__(kThreads) march_pcg_rqs_kernel(PH ph, Geo g, M
   constexpr int NP = 5;
   __shared__ double scratch[NP * kWarps];
   __shared__ __align__(16) double ring[kWarps * RqRing<PH::NC, A>::WARP];
+  pdl_wait();  // launched with launch_pdl: the previous iteration's pass must be done
   const int rhs = blockIdx.z;
   const lsg_pcg_scalars &s = a.scal[rhs];
   if (s.done != 0.0) return;

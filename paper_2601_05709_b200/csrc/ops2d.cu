@@ -330,7 +330,8 @@ static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_
   a.seg = seg_for(g, k, ctas_per_sm, a.nstrips);
   const dim3 grid((unsigned)ceil_div(a.nstrips, kWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
                   (unsigned)k);
-  march_pcg_rqs_kernel<PH, A><<<grid, kThreads, 0, st>>>(ph, g, a);
+  if (launch_pdl(march_pcg_rqs_kernel<PH, A>, grid, dim3(kThreads), 0, st, ph, g, a) != cudaSuccess)
+    return check_launch("march2d_pcg_rq launch");
   return check_launch("march2d_pcg_rq");
 }
 

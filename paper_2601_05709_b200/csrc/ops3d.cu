@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(kEwThreads)
     pcg_update(int64_t n, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
                double *partials, uint32_t *counters) {
   __shared__ double scratch[2 * (kEwThreads / 32)];
+  pdl_wait();
   const int rhs = blockIdx.y;
   lsg_pcg_scalars &s = scal[rhs];
   if (s.done != 0.0) return;
@@ -567,6 +568,7 @@ __global__ void __launch_bounds__(kEwThreads)
 __global__ void __launch_bounds__(kEwThreads, 4)  // 4 CTAs/SM: the grid is one full wave
     pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old,
              const double *p_old2, double *p_new, double *x, const lsg_pcg_scalars *scal) {
+  pdl_wait();
   const int rhs = blockIdx.y;
   const lsg_pcg_scalars &s = scal[rhs];
   if (s.done != 0.0) return;
@@ -976,7 +978,12 @@ static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   dim3 grid;
   launch_geometry(g, k, ctas, a.seg, a.nzseg, grid);
   a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
-  march3s<PH, ACT><<<grid, kThreads, smem, st>>>(ph, g, a);
+  if (ACT == PCGQ) {
+    if (launch_pdl(march3s<PH, ACT>, grid, dim3(kThreads), smem, st, ph, g, a) != cudaSuccess)
+      return check_launch("march3d launch");
+  } else {
+    march3s<PH, ACT><<<grid, kThreads, smem, st>>>(ph, g, a);
+  }
   return check_launch("march3d");
 }
 
@@ -1061,14 +1068,19 @@ static int iterate_once(const lsg_op &op, const lsg_pcg_ws &ws, int parity, int6
   const int ph = parity;  // iteration index mod 3 = slot of the new direction
   double *p_new = ring[ph], *p_old = ring[ph == 0 ? 2 : ph - 1];
   double *p_old2 = ring[ph == 2 ? 0 : ph + 1];
-  pcg_prep<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, p_old, p_old2, p_new, ws.x, ws.scal);
+  if (launch_pdl(pcg_prep, eg, dim3(kEwThreads), 0, st, n, ws.dinv, (const double *)ws.r,
+                 (const double *)p_old, (const double *)p_old2, p_new, ws.x,
+                 (const lsg_pcg_scalars *)ws.scal) != cudaSuccess)
+    return check_launch("pcg_prep3d launch");
   int rc = check_launch("pcg_prep3d");
   if (rc) return rc;
   if (after_prep && cudaEventRecord(after_prep, st) != cudaSuccess) return check_launch("event");
   a.x = p_new;
   rc = dispatch<PCGQ>(op, a, ws.k, st);
   if (rc) return rc;
-  pcg_update<<<eg, kEwThreads, 0, st>>>(n, ws.dinv, ws.r, ws.q, ws.scal, ws.partials, ws.counters);
+  if (launch_pdl(pcg_update, eg, dim3(kEwThreads), 0, st, n, ws.dinv, ws.r, (const double *)ws.q,
+                 ws.scal, ws.partials, ws.counters) != cudaSuccess)
+    return check_launch("pcg_update3d launch");
   return check_launch("pcg_update3d");
 }
 
