@@ -99,8 +99,20 @@ struct Elast {
   __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
                                        const double *u11, uint32_t word, int, int, double *c00,
                                        double *c10, double *c01, double *c11) const {
+    double wl, wu;
+    weights(word, wl, wu);
+    cell_w(u00, u10, u01, u11, wl, wu, c00, c10, c01, c11);
+  }
+  // element weights of the cell's lower / upper triangle (0 for invalid cells)
+  __device__ __forceinline__ void weights(uint32_t word, double &wl, double &wu) const {
     const double v = valid(word) ? 1.0 : 0.0;
-    const double wl = wof(word & 3u) * v, wu = wof((word >> 2) & 3u) * v;
+    wl = wof(word & 3u) * v;
+    wu = wof((word >> 2) & 3u) * v;
+  }
+  // the cell with its weights given (shared by several right-hand sides)
+  __device__ __forceinline__ void cell_w(const double *u00, const double *u10, const double *u01,
+                                         const double *u11, double wl, double wu, double *c00,
+                                         double *c10, double *c01, double *c11) const {
     double ALx, ALy, BLx, BLy, AUx, AUy, BUx, BUy;
     // lower (a=00, b=10, c=11): dP = u10 - u00, dQ = u11 - u10
     tri(u10[0] - u00[0], u10[1] - u00[1], u11[0] - u10[0], u11[1] - u10[1], wl, ALx, ALy, BLx, BLy);
@@ -145,8 +157,20 @@ struct Lap {
   __device__ __forceinline__ void cell(const double *u00, const double *u10, const double *u01,
                                        const double *u11, uint32_t word, int, int, double *c00,
                                        double *c10, double *c01, double *c11) const {
+    double wl, wu;
+    weights(word, wl, wu);
+    cell_w(u00, u10, u01, u11, wl, wu, c00, c10, c01, c11);
+  }
+  // element weights of the cell's lower / upper triangle (0 for invalid cells)
+  __device__ __forceinline__ void weights(uint32_t word, double &wl, double &wu) const {
     const double v = valid(word) ? 1.0 : 0.0;
-    const double wl = wof(word & 3u) * v, wu = wof((word >> 2) & 3u) * v;
+    wl = wof(word & 3u) * v;
+    wu = wof((word >> 2) & 3u) * v;
+  }
+  // the cell with its weights given (shared by several right-hand sides)
+  __device__ __forceinline__ void cell_w(const double *u00, const double *u10, const double *u01,
+                                         const double *u11, double wl, double wu, double *c00,
+                                         double *c10, double *c01, double *c11) const {
     const double XL = wl * ihx2 * (u10[0] - u00[0]), YL = wl * ihy2 * (u11[0] - u10[0]);
     const double XU = wu * ihx2 * (u11[0] - u01[0]), YU = wu * ihy2 * (u01[0] - u00[0]);
     c00[0] = -XL - YU;

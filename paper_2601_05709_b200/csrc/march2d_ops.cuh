@@ -954,6 +954,129 @@ __global__ void __launch_bounds__(kThreads) march_pcg_rqs_kernel(PH ph, Geo g, M
   }
 }
 
+// ----------------------------------------------------------------------------
+// The elasticity apply for two right-hand sides per warp (k >= 2): the same
+// march as march_core<Elast, APPLY>, with the word, the element weights and
+// the Dirichlet mask of a cell row formed once for both fields, and two
+// independent dependency chains per warp (the one-field apply is latency-
+// bound on short row segments).  Odd k: the last pair's second field is the
+// first one again, computed but not stored.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) apply2_kernel(Elast ph, Geo g, MArgs a, int k) {
+  constexpr int NC = 2, NOUT = 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = blockIdx.x * kWarps + warp;
+  const uint8_t *words = static_cast<const uint8_t *>(a.words);
+  const int nx = g.nx, ny = g.ny;
+  const int64_t nxp = nx + 1;
+  const int64_t nn = nxp * (ny + 1);
+  const int r0 = 2 * (int)blockIdx.z;
+  const bool two = r0 + 1 < k;
+  const int rr[2] = {r0, two ? r0 + 1 : r0};
+  const int i = strip * kStrip - 1 + lane;
+  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
+  const bool own = node_ok && lane >= 1 && lane <= kStrip;
+  const int ic = min(max(i, 0), nx);
+  const int J0 = blockIdx.y * a.seg;
+  const int J1 = min(J0 + a.seg, ny + 1);
+  const double *xin[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) xin[j] = a.x + (size_t)rr[j] * (size_t)nn * NC + (size_t)ic * NC;
+  const uint8_t *win = words + ic;
+
+  struct Raw {
+    double v[2][NC];
+    uint32_t wc;
+  };
+  struct Row {
+    double in[2][NC], rt[2][NC], raw[2][NC];
+    uint32_t wc;
+  };
+  auto fetch = [&](int r, Raw &f) {
+    const int64_t off = (int64_t)r * nxp;
+    f.wc = node_ok ? (uint32_t)__ldg(win + off) : 0u;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) ldg_node<NC>(xin[j], off, f.v[j]);
+  };
+  auto prepare = [&](const Raw &f, Row &S) {
+    S.wc = f.wc;
+    const uint32_t m = Elast::mask(f.wc);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        S.raw[j][c] = f.v[j][c];
+        S.in[j][c] = ((m >> c) & 1u) ? 0.0 : f.v[j][c];
+      }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) S.rt[j][c] = __shfl_down_sync(0xffffffffu, S.in[j][c], 1);
+  };
+  auto emit = [&](int r, const Row &S, const double (*accv)[NOUT]) {
+    const int64_t node = (int64_t)r * nxp + i;
+    const uint32_t m = Elast::mask(S.wc);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (j == 1 && !two) break;
+      double yv[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) yv[c] = ((m >> c) & 1u) ? S.raw[j][c] : accv[j][c];
+      st_node<NC>(a.y + (size_t)rr[j] * (size_t)nn * NC, node, yv);
+    }
+  };
+  auto step = [&](int r, const Raw &f, const Row &Sp, Row &Sn, double (*ap)[NOUT], double (*an)[NOUT]) {
+    prepare(f, Sn);
+    double wl, wu;
+    ph.weights(Sp.wc, wl, wu);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
+      ph.cell_w(Sp.in[j], Sp.rt[j], Sn.in[j], Sn.rt[j], wl, wu, c00, c10, c01, c11);
+#pragma unroll
+      for (int t = 0; t < NOUT; ++t) {
+        double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);
+        double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
+        if (lane == 0) up10 = up11 = 0.0;
+        ap[j][t] += c00[t] + up10;
+        an[j][t] = c01[t] + up11;
+      }
+    }
+    if (own && (r - 1) >= J0) emit(r - 1, Sp, ap);
+  };
+
+  const int jstart = max(J0 - 1, 0);
+  const int rend = min(J1, ny);
+  Row SA, SB;
+  double accA[2][NOUT], accB[2][NOUT];
+  Raw fA, fB;
+  {
+    Raw f0;
+    fetch(jstart, f0);
+    fetch(min(jstart + 1, rend), fA);
+    fetch(min(jstart + 2, rend), fB);
+    prepare(f0, SA);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) accA[j][t] = 0.0;
+  bool last_in_b = false;
+  int r = jstart + 1;
+  while (r <= rend) {
+    step(r, fA, SA, SB, accA, accB);
+    fetch(min(r + 2, rend), fA);
+    if (++r > rend) { last_in_b = true; break; }
+    step(r, fB, SB, SA, accB, accA);
+    fetch(min(r + 2, rend), fB);
+    ++r;
+  }
+  if (J1 == ny + 1 && own && ny >= J0) {
+    if (last_in_b) emit(ny, SB, accB);
+    else emit(ny, SA, accA);
+  }
+}
+
 template <class PH, int ACT, class W>
 __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   constexpr int NP = Traits<PH, ACT>::NP;

@@ -368,11 +368,36 @@ static int dispatch_op(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   return LSG_ERR_ARG;
 }
 
+// Two fields per warp for batched elasticity applies (L2 flushed: cfg2 k = 8
+// 23.5 -> 22.5 us, 2048x1024 k = 2 39.0 -> 35.8 us); LSG_APPLY2=0 keeps one.
+static bool apply2_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_APPLY2");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st) {
   MArgs a = {};
   a.words = op.words;
   a.x = x;
   a.y = y;
+  // even k only: an odd batch would carry a duplicate field (measured slower at k = 3)
+  if (op.kind == LSG_OP_ELASTICITY && k >= 2 && k % 2 == 0 && apply2_on()) {
+    const Geo g = geo_of(op.grid);
+    static int ctas_per_sm = -1;
+    if (ctas_per_sm < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                               &ctas_per_sm, apply2_kernel, kThreads, 0) != cudaSuccess)
+      ctas_per_sm = 4;
+    const int kp = (k + 1) / 2;
+    a.seg = seg_for(g, kp, ctas_per_sm);
+    a.nstrips = nstrips_of(g);
+    const dim3 grid = march_grid(g, a.seg, kp);
+    apply2_kernel<<<grid, kThreads, 0, st>>>(make_elast(g, op), g, a, k);
+    return check_launch("apply2_2d");
+  }
   return dispatch_op<APPLY>(op, a, k, st);
 }
 
