@@ -531,10 +531,12 @@ constexpr int kPcgFields = 5;  // r, p, q, M^-1, x
 template <class PH, bool COH = false>
 __device__ __forceinline__ void march_pcg(const PH &ph, const Geo &g, const MArgs &a, int bx,
                                           int by, int rhs, bool first, double beta,
-                                          double alpha_prev, double (&part)[5]) {
+                                          double alpha_prev, double (&part)[5],
+                                          int warp_in_task = -1) {
   constexpr int NC = PH::NC, NOUT = PH::NOUT, D = kPcgDepth;
   static_assert(PH::NIN == NC, "PCG operators read one field");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int warp = warp_in_task >= 0 ? warp_in_task : (int)(threadIdx.x >> 5);
   const int strip = bx * kWarps + warp;
   const uint8_t *words = static_cast<const uint8_t *>(a.words);
   const int nx = g.nx, ny = g.ny;

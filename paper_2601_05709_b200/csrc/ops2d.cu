@@ -566,6 +566,178 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ----------------------------------------------------------------------------
+// Cluster PCG for the smallest systems (<= kClusterCtas * kTasksPerCta marching
+// tasks, e.g. cfg1): one thread-block cluster of 16 CTAs runs every iteration
+// of a chunk.  Each CTA holds 3 tasks (12 warps); per iteration the warps' sums
+// are combined in fixed order in shared memory, the 16 CTA sums are read by
+// every CTA through distributed shared memory in rank order (same totals, same
+// decisions everywhere) and one cluster barrier per iteration replaces the
+// grid-wide barrier and the global partials of the cooperative kernel.  The
+// CTA sums alternate between two buffers by iteration (a CTA that runs ahead
+// cannot overwrite sums another CTA is still reading).  Data written in one
+// iteration and read (halo) by other CTAs in the next is ordered by the
+// barrier's release/acquire at cluster scope.
+// ----------------------------------------------------------------------------
+constexpr int kClusterCtas = 16;
+constexpr int kTasksPerCta = 3;
+
+template <class PH, int KMAX>
+__global__ void __launch_bounds__(kThreads * kTasksPerCta, 1)
+    pcg_cluster(PH ph, Geo g, MArgs a, int k, int tx, int ty, int niter, int parity0,
+                double *r_even, double *r_odd, double *p_even, double *p_odd, double *q_even,
+                double *q_odd) {
+  constexpr int NS = kPcgSums;
+  constexpr int NW = kWarps * kTasksPerCta;
+  constexpr int NV = KMAX * NS;
+  cgrp::cluster_group cl = cgrp::this_cluster();
+  __shared__ double s_warp[NW][NV];
+  __shared__ double s_cta[2][NV];
+  __shared__ lsg_pcg_scalars s_sc[KMAX];
+  __shared__ int s_all;
+  const int rank = (int)cl.block_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / kWarps, wt = warp % kWarps;
+  for (int t = threadIdx.x; t < KMAX; t += blockDim.x) {
+    if (t < k) s_sc[t] = a.scal[t];
+    else s_sc[t].done = 1.0;
+  }
+  __syncthreads();
+  int parity = parity0;
+  const int ntask = tx * ty * k;
+  const int nslot = kClusterCtas * kTasksPerCta;
+  for (int it = 0; it < niter; ++it, parity ^= 1) {
+    if (threadIdx.x == 0) {
+      int all = 1;
+      for (int r = 0; r < KMAX; ++r) all &= s_sc[r].done != 0.0;
+      s_all = all;
+    }
+    for (int t = threadIdx.x; t < NW * NV; t += blockDim.x) (&s_warp[0][0])[t] = 0.0;
+    __syncthreads();
+    if (s_all) break;  // identical in every CTA of the cluster
+    MArgs aa = a;
+    aa.x = parity ? r_odd : r_even;
+    aa.y3 = parity ? r_even : r_odd;
+    aa.x2 = parity ? p_odd : p_even;
+    aa.y2 = parity ? p_even : p_odd;
+    aa.x3 = parity ? q_odd : q_even;
+    aa.y = parity ? q_even : q_odd;
+    for (int t = rank * kTasksPerCta + slot; t < ntask; t += nslot) {
+      const int rhs = t / (tx * ty), rem = t - rhs * (tx * ty);
+      const lsg_pcg_scalars &sc = s_sc[rhs];
+      if (sc.done != 0.0) continue;  // uniform across the task's warps
+      double part[NS];
+#pragma unroll
+      for (int v = 0; v < NS; ++v) part[v] = 0.0;
+      march_pcg<PH, true>(ph, g, aa, rem % tx, rem / tx, rhs, sc.first != 0.0, sc.beta, sc.alpha,
+                          part, wt);
+#pragma unroll
+      for (int v = 0; v < NS; ++v) {
+        const double w = warp_sum(part[v]);
+        if (lane == 0) s_warp[warp][rhs * NS + v] += w;
+      }
+    }
+    __syncthreads();
+    double *mine = s_cta[it & 1];
+    for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += s_warp[w][v];
+      mine[v] = acc;
+    }
+    cl.sync();  // every CTA's sums (and this iteration's vectors) are published
+    if (threadIdx.x < NV) {
+      double tot = 0.0;
+      for (int c = 0; c < kClusterCtas; ++c) tot += cl.map_shared_rank(mine, c)[threadIdx.x];
+      s_warp[0][threadIdx.x] = tot;  // reuse: totals per (rhs, sum)
+    }
+    __syncthreads();
+    if (threadIdx.x < KMAX) {
+      const int r = threadIdx.x;
+      if (r < k && s_sc[r].done == 0.0) {
+        pcg_decide(s_sc[r], &s_warp[0][r * NS]);
+        if (rank == 0) a.scal[r] = s_sc[r];
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA exits while another may still read its shared memory
+}
+
+template <class PH, int KMAX>
+static int launch_cluster_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws, int niter,
+                            cudaStream_t st) {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = 0;
+    if (cudaFuncSetAttribute(pcg_cluster<PH, KMAX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kClusterCtas);
+      cfg.blockDim = dim3(kThreads * kTasksPerCta);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kClusterCtas;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, pcg_cluster<PH, KMAX>, &cfg) == cudaSuccess &&
+          nclusters >= 1)
+        ok = 1;
+    }
+    cudaGetLastError();  // clear any error of the probe
+  }
+  if (!ok) return 1;
+  int k = ws.k, tx = (int)0, ty = 0, parity = ws.parity;
+  double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
+  a.nstrips = nstrips_of(g);
+  a.seg = seg_for(g, ws.k, 3);
+  const dim3 mg = march_grid(g, a.seg, ws.k);
+  tx = (int)mg.x;
+  ty = (int)mg.y;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCtas);
+  cfg.blockDim = dim3(kThreads * kTasksPerCta);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kClusterCtas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, pcg_cluster<PH, KMAX>, ph, g, a, k, tx, ty, niter, parity, re, ro, pe, po,
+                         qe, qo) != cudaSuccess)
+    return check_launch("pcg_cluster");
+  ws.parity ^= (niter & 1);
+  return check_launch("pcg_cluster");
+}
+
+// LSG_PCG2D_CLUSTER=0 keeps the cooperative persistent kernel for small systems.
+static bool cluster_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_PCG2D_CLUSTER");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// 1 = not applicable (too many tasks, or no cluster of 16 fits): use another path
+template <class PH>
+static int launch_cluster(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws, int niter,
+                          cudaStream_t st) {
+  if (!cluster_on()) return 1;
+  const int seg = seg_for(g, ws.k, 3);
+  const dim3 mg = march_grid(g, seg, ws.k);
+  if ((int64_t)mg.x * mg.y * ws.k > (int64_t)kClusterCtas * kTasksPerCta) return 1;
+  if (ws.k == 1) return launch_cluster_k<PH, 1>(ph, g, a, ws, niter, st);
+  if (ws.k <= 4) return launch_cluster_k<PH, 4>(ph, g, a, ws, niter, st);
+  if (ws.k <= 8) return launch_cluster_k<PH, 8>(ph, g, a, ws, niter, st);
+  return 1;
+}
+
 // LSG_PCG2D_PERSISTENT=0 keeps the two-kernel (graph-replayed) iteration.
 static bool persistent_on() {
   static int v = -1;
@@ -664,6 +836,10 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   a.xs = ws.x;
   if (pcg_persistent_ok(op, ws)) {
     int rc = 1;
+    if (op.kind == LSG_OP_ELASTICITY) rc = launch_cluster<Elast>(make_elast(g, op), g, a, ws, niter, st);
+    else if (op.kind == LSG_OP_H1) rc = launch_cluster<H1>(make_h1(g, op), g, a, ws, niter, st);
+    else rc = launch_cluster<Lap>(make_lap(g, op), g, a, ws, niter, st);
+    if (rc <= 0) return rc;
     if (op.kind == LSG_OP_ELASTICITY) rc = launch_persistent<Elast>(make_elast(g, op), g, a, ws, niter, st);
     else if (op.kind == LSG_OP_H1) rc = launch_persistent<H1>(make_h1(g, op), g, a, ws, niter, st);
     else rc = launch_persistent<Lap>(make_lap(g, op), g, a, ws, niter, st);
