@@ -15,6 +15,9 @@
   one batched launch (replacing the thread pool of ``driver.py:169-194``).
 """
 
+import itertools
+import os
+
 import numpy as np
 import torch
 
@@ -315,7 +318,52 @@ def _scal(ws, field):
     return ws.host_scal[:, _lib.SCAL_FIELDS.index(field)]
 
 
-def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, chunk=32):
+# Iterations the previous solve of the same kind of system needed (max over its
+# right-hand sides): the optimisation loop solves warm-started systems whose
+# counts change slowly, so the next solve is enqueued as one chunk of ~90% of
+# that count and then short chunks, instead of doubling chunks that overshoot
+# convergence by up to one chunk of no-op iterations and poll the host ~8 times
+# (a chunk is enqueued as power-of-two launches without polling in between).
+# Chunking never changes the iterates (the device decides convergence per
+# iteration); it only sets how often the host polls.
+_LAST_ITERS = {}
+_CHUNK_DOUBLING = os.environ.get("LSG_CHUNK_DOUBLING") == "1"  # A/B: the plain doubling plan
+
+
+def _pieces(total):
+    """A chunk as power-of-two launches of 32..512 iterations (the CUDA-graph cache
+    keys on the iteration count, so only five shapes are ever captured)."""
+    out = []
+    while total >= 32:
+        p = 512
+        while p > total:
+            p //= 2
+        out.append(p)
+        total -= p
+    return out or [32]
+
+
+def _chunks(last):
+    """Chunk sizes for a solve whose predecessor needed `last` iterations."""
+    if not last:
+        c = 32
+        while True:
+            yield c
+            c = min(2 * c, 512)
+    first = max(32, int(0.9 * last))
+    yield first
+    step = max(32, last // 16)
+    done = first
+    while done < 1.5 * last:
+        yield step
+        done += step
+    c = step
+    while True:  # far beyond the previous count: back to doubling
+        c = min(2 * c, 512)
+        yield c
+
+
+def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, chunk=None):
     """Jacobi-PCG on k right-hand sides sharing ``op``; returns (x (k, n), iterations (k,)).
 
     scipy ``cg`` semantics per right-hand side: threshold max(atol, rtol ||b||),
@@ -346,12 +394,19 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
     ev.synchronize()
     done = _scal(ws, "done")
     prof = PCG_PROFILE
+    key = (op.kind, id(op.space.mesh), n, k, float(rtol))
+    if chunk is not None:
+        plan = itertools.repeat(int(chunk))
+    else:
+        plan = _chunks(None if _CHUNK_DOUBLING else _LAST_ITERS.get(key))
     while not bool((done != 0).all()):
+        chunk = next(plan)
         if prof is not None:
             before = _scal(ws, "iters").clone()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        _lib.call("lsg_pcg_iterate", cop, ws.ws, int(chunk), st)
+        for piece in _pieces(chunk):  # power-of-two launches: a handful of graph shapes
+            _lib.call("lsg_pcg_iterate", cop, ws.ws, int(piece), st)
         if prof is not None:
             e1.record(stream)
         ws.host_scal.copy_(ws.scal, non_blocking=True)
@@ -362,9 +417,9 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
             delta = _scal(ws, "iters") - before
             prof.append(dict(kind=op.kind, k=k, n=n, events=(e0, e1), launched=int(chunk),
                              rhs_iters=float(delta.sum()), max_iters=float(delta.max())))
-        chunk = min(chunk * 2, 512)
     _lib.call("lsg_pcg_finish", cop, ws.ws, st)  # pending x += alpha p of the last iteration
     iters = _scal(ws, "iters").to(torch.int64).clone()
+    _LAST_ITERS[key] = int(iters.max())
     failed = (done == 2).nonzero().flatten().tolist()
     x = ws.x.clone()
     if failed:
