@@ -928,7 +928,8 @@ static H1P make_h1_plain(const Geo &g, const lsg_op &op) {
 
 int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 
-static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
+static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid,
+                            int default_waves = 3) {
   const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
   const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
   // z-segments (one halo plane each) sized for ~3 waves of CTAs and at most
@@ -939,10 +940,10 @@ static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int 
   static int waves = -1;  // LSG_M3_WAVES: target waves of CTAs (experiments)
   if (waves < 0) {
     const char *e = getenv("LSG_M3_WAVES");
-    waves = e ? atoi(e) : 3;
-    if (waves < 1) waves = 1;
+    waves = e ? atoi(e) : 0;
   }
-  int64_t ns = ceil_div(waves * slots, per_seg);
+  const int64_t wv = waves > 0 ? waves : default_waves;
+  int64_t ns = ceil_div(wv * slots, per_seg);
   if (ns < 1) ns = 1;
   int64_t s = ceil_div(g.nz + 1, ns);
   static int smax = -1;  // LSG_M3_SEGMAX: cap on planes per segment (experiments)
@@ -976,7 +977,9 @@ static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
       ctas = 2;
   }
   dim3 grid;
-  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid);
+  // the PCG stencil runs beside the other half-batch's elementwise passes (two
+  // streams): 2 waves of longer segments measured better there (cfg5 472 -> 466 us)
+  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid, ACT == PCGQ ? 2 : 3);
   a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
   if (ACT == PCGQ) {
     if (launch_pdl(march3s<PH, ACT>, grid, dim3(kThreads), smem, st, ph, g, a) != cudaSuccess)
