@@ -773,6 +773,13 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
       segmin = e ? atoi(e) : 0;
     }
     if (a.seg < segmin) a.seg = segmin;
+    // mid-size systems: 8-row tasks while that still gives every SM one (velocity
+    // solve of cfg2, 1024x256: 14.5 -> 13.2 us; 512x256: 12.3 -> 10.8 us); with fewer
+    // tasks the longer march costs more than the barriers it saves (320x160: 7.9 vs 9.1)
+    if (a.seg < 8) {
+      const dim3 m8 = march_grid(g, 8, ws.k);
+      if ((int64_t)m8.x * m8.y * ws.k >= kSMs) a.seg = 8;
+    }
   }
   a.nstrips = nstrips_of(g);
   const dim3 mg = march_grid(g, a.seg, ws.k);
