@@ -50,11 +50,73 @@ def parse():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-largest", action="store_true",
+                    help="skip the apply measurements on the largest 2D / 3D meshes (cfg4, cfg5)")
     ap.add_argument("--shard-loads", action="store_true",
                     help="N > 1: split the load cases across GPUs (strong scaling, one NCCL "
                          "all-reduce of J and the derivative vector per iteration) instead of "
                          "running independent replicas")
     return ap.parse_args()
+
+
+def largest_applies(hbm, fp64_peak):
+    """The north star's apply gate on the largest meshes: cfg4 (2D, 4096x2048, k = 1) and
+    cfg5 (3D, 192x96x96 Kuhn tets, k = 4), random two-phase material, clamped x = 0,
+    L2 flushed (256 MB write + read) before each launch.  Bytes: 16 d k N + material."""
+    import torch
+
+    from paper_2601_05709_b200 import build_box_mesh, build_rect_mesh
+    from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace
+
+    out = {}
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    clean = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for name, dim, n, k in (("cfg4", 2, (4096, 2048), 1), ("cfg5", 3, (192, 96, 96), 4)):
+        rule = [(1, lambda p: p[:, 0] < 1e-12)]
+        if dim == 2:
+            mesh = build_rect_mesh((0.0, 0.0, 2.0, 1.0), n[0], n[1], rule)
+            lame = (0.3 / 0.91, 1.0 / 2.6)
+        else:
+            mesh = build_box_mesh((0.0, 0.0, 0.0, 2.0, 1.0, 1.0), n, rule)
+            lame = (0.3 / (1.3 * 0.4), 1.0 / 2.6)
+        N, E = mesh.num_vertices, mesh.num_elements
+        space = FunctionSpace(mesh, dim)
+        phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
+        op = ElasticityOperator(space, phi, lame, 1e-3, DirichletSet.on_tags(space, 1))
+        u = torch.randn((k, dim * N), dtype=torch.float64, device="cuda")
+        op.apply(u)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(100_000_000)
+        evs = []
+        for rep in range(13):
+            flush.fill_(float(rep))
+            clean.sum()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            op.apply(u)
+            a1.record(stream)
+            if rep >= 3:
+                evs.append((a0, a1))
+        torch.cuda.synchronize()
+        t = statistics.median([e0.elapsed_time(e1) / 1e3 for e0, e1 in evs])
+        byts = 16.0 * dim * k * N + (E if dim == 2 else 4.0 * N)
+        out[name] = {"grid": "x".join(map(str, n)), "k": k, "ms": t * 1e3,
+                     "dof_per_s": k * dim * N / t, "gbs": byts / t / 1e9,
+                     "frac": byts / t / 1e9 / hbm, "bytes": byts}
+        del op, u
+    # Kuhn-tet stencil: ~220 fp64 instructions per cell and field (DESIGN.md section 3)
+    cells = 192 * 96 * 96
+    lanes = 220.0 * cells * 4
+    t_fp64 = lanes / ((fp64_peak or 34.172e12) / 2)  # DFMA lane-ops/s = FLOP/s / 2
+    out["cfg5"]["fp64_bound_ms"] = t_fp64 * 1e3
+    out["cfg5"]["fp64_pipe_frac"] = t_fp64 / (out["cfg5"]["ms"] / 1e3)
+    out["cfg5"]["note"] = ("fp64-issue-bound: ~220 fp64 instructions per cell and field need %.0f us "
+                           "at the measured fp64 peak, which caps the HBM fraction near 0.6 even at "
+                           "100%% of the fp64 pipe; fp64_pipe_frac is this op count over the "
+                           "measured time" % (t_fp64 * 1e6))
+    del flush, clean
+    return out
 
 
 def ncu_traffic():
@@ -304,6 +366,16 @@ def b200_arm(args, world, rank, local):
     del flush, clean
     apply_bytes = 16.0 * d * k * N + E
 
+    largest = None
+    if not args.no_largest and rank == 0:
+        fp64 = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
+                fp64 = float(json.load(f)["fp64_tflops"]) * 1e12
+        except Exception:
+            fp64 = None
+        largest = largest_applies(hbm, fp64)
+
     # ---- end to end through the public API from host buffers ----------------------------
     e2e = None
     if not args.no_e2e:
@@ -393,6 +465,7 @@ def b200_arm(args, world, rank, local):
                       "flush": "256 MB write + 256 MB read of another buffer before each launch "
                                "(ms_dirty_flush: write only; the flush's dirty lines are then "
                                "written back during the timed launch)"},
+            "apply_largest": largest,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
