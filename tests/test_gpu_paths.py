@@ -1,10 +1,10 @@
-"""The three ways a 2D PCG chunk can run -- the persistent cooperative kernel
-(small systems), the CUDA-graph replay of the two-kernel iteration, and
-direct launches, and the stored-q variant of the single pass
-(LSG_PCG2D_RQ=0) beside the default one that recomputes q_{i-1} -- give the same solutions, including right-hand sides that
-converge in the middle of a chunk (their pending x updates are applied by the
-next pass A or by lsg_pcg_finish).  Each path runs in its own process because
-the switches are read once per process.  Needs a B200."""
+"""The ways a 2D PCG chunk can run give the same solutions: the 16-CTA cluster
+kernel and the cooperative persistent kernel (small systems), CUDA-graph
+replays and direct launches of the per-launch single pass, and its stored-q
+variant (LSG_PCG2D_RQ=0) beside the default recompute-q pass -- including
+right-hand sides that converge in the middle of a chunk and a zero right-hand
+side.  Each path runs in its own process because the switches are read once
+per process.  Needs a B200."""
 
 import json
 import os
@@ -69,7 +69,9 @@ def test_pcg_paths_agree(tmp_path):
     xg, itg, tg = run_path(tmp_path, "graph", {"LSG_PCG2D_PERSISTENT": "0"})
     xd, itd, td = run_path(tmp_path, "direct", {"LSG_PCG2D_PERSISTENT": "0", "LSG_NO_GRAPHS": "1"})
     xq, itq, tq = run_path(tmp_path, "storedq", {"LSG_PCG2D_PERSISTENT": "0", "LSG_PCG2D_RQ": "0"})
-    for x, res in (tp, tg, td, tq):  # every path meets the stopping rule in the true residual
+    # small systems default to the 16-CTA cluster kernel; this is the cooperative one
+    xc, itc, tc = run_path(tmp_path, "coop", {"LSG_PCG2D_CLUSTER": "0"})
+    for x, res in (tp, tg, td, tq, tc):  # every path meets the stopping rule in the true residual
         assert (res <= 1e-10).all(), res
     assert np.linalg.norm(tp[0] - tg[0]) <= 1e-10 * np.linalg.norm(tg[0])
     assert itp[2] == itg[2] == itd[2] == 0 and not xp[2].any() and not xg[2].any()
@@ -80,6 +82,10 @@ def test_pcg_paths_agree(tmp_path):
     for r in range(2):
         assert abs(itq[r] - itg[r]) <= max(2, itg[r] // 50)
         assert np.linalg.norm(xq[r] - xg[r]) <= 1e-8 * np.linalg.norm(xg[r])
+    assert itc[2] == 0 and not xc[2].any()
+    for r in range(2):  # cluster vs cooperative: same pass, other reduction grouping
+        assert abs(itc[r] - itp[r]) <= max(2, itp[r] // 50)
+        assert np.linalg.norm(xc[r] - xp[r]) <= 1e-8 * np.linalg.norm(xp[r])
     for r in range(2):
         assert itp[r] > 10 and abs(itp[r] - itg[r]) <= max(2, itp[r] // 20)
         assert np.linalg.norm(xp[r] - xg[r]) <= 1e-8 * np.linalg.norm(xg[r])
