@@ -1136,15 +1136,21 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     return dim3((unsigned)(need < slots ? need : slots), (unsigned)k);
   };
   if (streams3d() == 2 && ws.k >= 2) {
-    static cudaStream_t st2 = nullptr;
-    static cudaEvent_t ev_fork = nullptr, ev_prep = nullptr, ev_join = nullptr;
-    if (!st2) {
-      if (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev_prep, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+    // library-owned second stream and events, one set per device
+    constexpr int kMaxDev = 64;
+    static cudaStream_t st2s[kMaxDev] = {};
+    static cudaEvent_t evs[kMaxDev][3] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return check_launch("pcg3d device");
+    if (!st2s[dev]) {
+      if (cudaStreamCreateWithFlags(&st2s[dev], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&evs[dev][0], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&evs[dev][1], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&evs[dev][2], cudaEventDisableTiming) != cudaSuccess)
         return check_launch("pcg3d streams");
     }
+    cudaStream_t st2 = st2s[dev];
+    cudaEvent_t ev_fork = evs[dev][0], ev_prep = evs[dev][1], ev_join = evs[dev][2];
     const int k1 = ws.k / 2, k2 = ws.k - k1;
     const lsg_pcg_ws w1 = sub_ws(ws, 0, k1, n), w2 = sub_ws(ws, k1, k2, n);
     const dim3 g1 = grid_for(k1), g2 = grid_for(k2);
