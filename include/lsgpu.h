@@ -121,7 +121,10 @@ typedef struct {
  * system persistent kernel and the stored-q variant.  3D runs an elementwise
  * pass that forms p, the stencil pass, and an update pass, with three
  * direction buffers (p, p_alt, p_ring); a batch of k >= 2 runs as two halves
- * on two library-owned streams joined back into the caller's stream.  `parity` (which buffers are current) is owned
+ * on two streams (the caller's and a library-owned one per device, joined back
+ * into the caller's stream).  lsg_pcg_iterate serialises its graph captures
+ * and launches behind one lock; with LSG_NO_GRAPHS=1, calls from several host
+ * threads on one device must not overlap.  `parity` (which buffers are current) is owned
  * by the library: lsg_pcg_start resets it, lsg_pcg_iterate advances it once
  * per iteration. */
 typedef struct {
