@@ -1,2 +1,2 @@
-VARIANTS=("base||" "smem120k|LSG_M3_PCGQ_SMEM=122880|" "smem120k_w1|LSG_M3_PCGQ_SMEM=122880 LSG_M3_WAVES=1|" "smem120k_w3|LSG_M3_PCGQ_SMEM=122880 LSG_M3_WAVES=3|")
-source tools/ab_var.sh "192x96x96 4 50;128x64x64 2 100"
+VARIANTS=("def||" "smin5|LSG_M3_SEGMIN=5|" "smin7|LSG_M3_SEGMIN=7|" "smin8|LSG_M3_SEGMIN=8|")
+source tools/ab_var.sh "96x48x48 1 300;192x96x96 4 50"
