@@ -1,2 +1,2 @@
-VARIANTS=("def||" "smin5|LSG_M3_SEGMIN=5|" "smin7|LSG_M3_SEGMIN=7|" "smin8|LSG_M3_SEGMIN=8|")
-source tools/ab_var.sh "96x48x48 1 300;192x96x96 4 50"
+VARIANTS=("def||" "smax33|LSG_M3_SEGMAX=33|" "smax49|LSG_M3_SEGMAX=49|" "smax33w2|LSG_M3_SEGMAX=33 LSG_M3_WAVES=2|")
+source tools/ab_var.sh "192x96x96 4 50"
