@@ -1081,6 +1081,129 @@ __global__ void __launch_bounds__(kThreads) apply2_kernel(Elast ph, Geo g, MArgs
   }
 }
 
+// ----------------------------------------------------------------------------
+// The apply with its prefetch ring in shared memory (per-lane cp.async of the
+// node's field and the aligned word chunk, kApplyAhead rows ahead, no
+// barriers: each lane reads back only its own copies).  Same march, same
+// arithmetic and summation order as march_core<PH, APPLY>; the register ring
+// of march_core holds only two rows because deeper register rings cost
+// resident CTAs.
+// ----------------------------------------------------------------------------
+#ifndef LSG_APPLY_AHEAD
+#define LSG_APPLY_AHEAD 6
+#endif
+constexpr int kApplyAhead = LSG_APPLY_AHEAD;
+
+template <class PH>
+__global__ void __launch_bounds__(kThreads) apply_s_kernel(PH ph, Geo g, MArgs a) {
+  constexpr int NC = PH::NC, NOUT = PH::NOUT, A = kApplyAhead, D = A + 1;
+  constexpr int FS = 32 * NC;        // doubles per slot: the field
+  constexpr int SLOT = FS + 16;      // + 32 words
+  __shared__ __align__(16) double ring_all[kWarps * D * SLOT];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = blockIdx.x * kWarps + warp;
+  const uint8_t *words = static_cast<const uint8_t *>(a.words);
+  const int nx = g.nx, ny = g.ny;
+  const int64_t nxp = nx + 1;
+  const int64_t nn = nxp * (ny + 1);
+  const int i = strip * kStrip - 1 + lane;
+  const bool node_ok = (strip < a.nstrips) && i >= 0 && i <= nx;
+  const bool own = node_ok && lane >= 1 && lane <= kStrip;
+  const int ic = min(max(i, 0), nx);
+  const int J0 = blockIdx.y * a.seg;
+  const int J1 = min(J0 + a.seg, ny + 1);
+  const size_t voff = (size_t)blockIdx.z * (size_t)nn * NC;
+  const double *xin = a.x + voff;
+  double *myring = ring_all + (size_t)warp * D * SLOT;
+
+  struct Row {
+    double in[NC], rt[NC], raw[NC];
+    uint32_t wc;
+  };
+  auto fetch = [&](int r, int sl) {
+    double *S = myring + sl * SLOT;
+    const int64_t node = (int64_t)r * nxp + ic;
+    if constexpr (NC == 2) cp_async16(S + lane * NC, xin + node * NC);
+    else cp_async8(S + lane * NC, xin + node * NC);
+    uint32_t *W = reinterpret_cast<uint32_t *>(S + FS);
+    const int64_t wq = node & ~(int64_t)3;
+    if (wq + 4 <= nn) cp_async4(W + lane, words + wq);
+    else W[lane] = (uint32_t)words[node] << (8 * (node & 3));
+    cp_async_commit();
+  };
+  auto prepare = [&](int r, int sl, Row &S) {
+    const double *P = myring + sl * SLOT;
+    const uint32_t w4 = reinterpret_cast<const uint32_t *>(P + FS)[lane];
+    const int64_t node = (int64_t)r * nxp + ic;
+    S.wc = node_ok ? (w4 >> (8 * (uint32_t)(node & 3))) & 0xffu : 0u;
+    const uint32_t m = PH::mask(S.wc);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      S.raw[c] = P[lane * NC + c];
+      S.in[c] = ((m >> c) & 1u) ? 0.0 : S.raw[c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) S.rt[c] = __shfl_down_sync(0xffffffffu, S.in[c], 1);
+  };
+  auto emit = [&](int r, const Row &S, const double *accv) {
+    const int64_t node = (int64_t)r * nxp + i;
+    const uint32_t m = PH::mask(S.wc);
+    double yv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) yv[c] = ((m >> c) & 1u) ? S.raw[c] : accv[c];
+    st_node<NC>(a.y + voff, node, yv);
+  };
+  auto step = [&](int r, int sl, const Row &Sp, Row &Sn, double *ap, double *an) {
+    cp_async_wait_all_but<A - 1>();  // row r has landed
+    prepare(r, sl, Sn);
+    double c00[NOUT], c10[NOUT], c01[NOUT], c11[NOUT];
+    ph.cell(Sp.in, Sp.rt, Sn.in, Sn.rt, Sp.wc, i, r - 1, c00, c10, c01, c11);
+#pragma unroll
+    for (int t = 0; t < NOUT; ++t) {
+      double up10 = __shfl_up_sync(0xffffffffu, c10[t], 1);
+      double up11 = __shfl_up_sync(0xffffffffu, c11[t], 1);
+      if (lane == 0) up10 = up11 = 0.0;
+      ap[t] += c00[t] + up10;
+      an[t] = c01[t] + up11;
+    }
+    if (own && (r - 1) >= J0) emit(r - 1, Sp, ap);
+  };
+
+  const int jstart = max(J0 - 1, 0);
+  const int rend = min(J1, ny);
+  auto nxt = [](int s) { return s + 1 == D ? 0 : s + 1; };
+  // rows jstart .. jstart + A in slots 0 .. A
+#pragma unroll
+  for (int s = 0; s < D; ++s) fetch(min(jstart + s, rend), s);
+  Row SA, SB;
+  double accA[NOUT], accB[NOUT];
+  cp_async_wait_all_but<D - 1>();
+  prepare(jstart, 0, SA);
+#pragma unroll
+  for (int t = 0; t < NOUT; ++t) accA[t] = 0.0;
+  bool last_in_b = false;
+  int r = jstart + 1, sl = 1;
+  // step r consumes slot sl (row r); the slot of row r - 1 is refilled with row r + A
+  int sfree = 0;
+  while (r <= rend) {
+    step(r, sl, SA, SB, accA, accB);
+    fetch(min(r + A, rend), sfree);
+    sfree = sl;
+    sl = nxt(sl);
+    if (++r > rend) { last_in_b = true; break; }
+    step(r, sl, SB, SA, accB, accA);
+    fetch(min(r + A, rend), sfree);
+    sfree = sl;
+    sl = nxt(sl);
+    ++r;
+  }
+  cp_async_wait_all_but<0>();
+  if (J1 == ny + 1 && own && ny >= J0) {
+    if (last_in_b) emit(ny, SB, accB);
+    else emit(ny, SA, accA);
+  }
+}
+
 template <class PH, int ACT, class W>
 __global__ void __launch_bounds__(kThreads) march(PH ph, Geo g, MArgs a) {
   constexpr int NP = Traits<PH, ACT>::NP;

@@ -368,6 +368,30 @@ static int dispatch_op(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   return LSG_ERR_ARG;
 }
 
+// The apply with a shared-memory prefetch ring (apply_s_kernel); LSG_APPLY_SMEM=0
+// keeps the register-ring march.
+static bool apply_s_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LSG_APPLY_SMEM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <class PH>
+static int launch_apply_s(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  static int ctas_per_sm = -1;
+  if (ctas_per_sm < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                             &ctas_per_sm, apply_s_kernel<PH>, kThreads, 0) != cudaSuccess)
+    ctas_per_sm = 4;
+  a.seg = seg_for(g, k, ctas_per_sm);
+  a.nstrips = nstrips_of(g);
+  const dim3 grid = march_grid(g, a.seg, k);
+  apply_s_kernel<PH><<<grid, kThreads, 0, st>>>(ph, g, a);
+  return check_launch("apply_s2d");
+}
+
 // Two fields per warp for batched elasticity applies (L2 flushed: cfg2 k = 8
 // 23.5 -> 22.5 us, 2048x1024 k = 2 39.0 -> 35.8 us); LSG_APPLY2=0 keeps one.
 static bool apply2_on() {
@@ -397,6 +421,13 @@ int apply(const lsg_op &op, int k, const double *x, double *y, cudaStream_t st) 
     const dim3 grid = march_grid(g, a.seg, kp);
     apply2_kernel<<<grid, kThreads, 0, st>>>(make_elast(g, op), g, a, k);
     return check_launch("apply2_2d");
+  }
+  if (k == 1 && apply_s_on()) {  // measured: cfg4 67.5 -> 65.5 us; batched fields do better
+                                 // with apply2 (even k) or the register ring (odd k)
+    const Geo g = geo_of(op.grid);
+    if (op.kind == LSG_OP_ELASTICITY) return launch_apply_s<Elast>(make_elast(g, op), g, a, k, st);
+    if (op.kind == LSG_OP_H1) return launch_apply_s<H1>(make_h1(g, op), g, a, k, st);
+    if (op.kind == LSG_OP_LAPLACE) return launch_apply_s<Lap>(make_lap(g, op), g, a, k, st);
   }
   return dispatch_op<APPLY>(op, a, k, st);
 }

@@ -73,6 +73,11 @@ def _elasticity(grid, mesh, phi, rng, lame, k=2):
     got = host(op.apply(torch.as_tensor(u, device="cuda")))
     for g, x in zip(got, u):
         assert rel_l2(g, K @ x) <= 1e-10
+    # single field (shared-memory-ring apply) and an odd batch (register-ring apply)
+    assert rel_l2(host(op.apply(torch.as_tensor(u[0], device="cuda"))), K @ u[0]) <= 1e-10
+    u3 = np.concatenate([u, u[:1] * -0.5])
+    for g, x in zip(host(op.apply(torch.as_tensor(u3, device="cuda"))), u3):
+        assert rel_l2(g, K @ x) <= 1e-10
     assert rel_l2(host(op.diagonal()), K.diagonal()) <= 1e-12
     bc = DirichletSet.on_tags(space, 1)
     np.testing.assert_array_equal(bc.dofs, clamp)
