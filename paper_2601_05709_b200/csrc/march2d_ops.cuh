@@ -711,7 +711,9 @@ __device__ __forceinline__ void march_pcg(const PH &ph, const Geo &g, const MArg
 // sharing words, weights, masks and M^-1 (168 registers, 3 CTAs/SM), 54.7 vs
 // 49.5 us on the same box; strength-reduced ring/row addressing, no change; a
 // per-CTA shared table of w(n) k_j instead of the weight arithmetic, 66.0 vs
-// 51.6 us -- lane-divergent table reads on the critical path.)
+// 51.6 us -- lane-divergent table reads on the critical path; branch-free
+// masked sums with predicated stores and two steps per basic block, 53.7 vs
+// 51.6 us.)
 // ----------------------------------------------------------------------------
 constexpr int kStripRq = 28;
 
