@@ -717,16 +717,14 @@ static int launch_cluster_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws,
           nclusters >= 1)
         ok = 1;
     }
-    cudaGetLastError();  // clear any error of the probe
+    cudaGetLastError();  // a failed probe (no 16-CTA cluster fits) only selects the fallback
   }
   if (!ok) return 1;
-  int k = ws.k, tx = (int)0, ty = 0, parity = ws.parity;
-  double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
   a.nstrips = nstrips_of(g);
   a.seg = seg_for(g, ws.k, 3);
   const dim3 mg = march_grid(g, a.seg, ws.k);
-  tx = (int)mg.x;
-  ty = (int)mg.y;
+  const int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
+  double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kClusterCtas);
   cfg.blockDim = dim3(kThreads * kTasksPerCta);
