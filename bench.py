@@ -418,6 +418,8 @@ def b200_arm(args, world, rank, local):
         v, t_outer = cpu_iters_per_sec(s, rhs_per_outer)
         cpu = {"value": v, "unit": "iters/s", "cores": 1, "kind": "port",
                "apply_dof_per_s": s["k"] * s["n"] / s["apply"],
+               "breakdown": {"assembly_s": s["asm"], "pcg_ms_per_rhs_iteration": s["cg"] / s["cg_rhs_iters"] * 1e3,
+                             "s1_and_rhs_s": s["s1"], "transport_s": s["transport"]},
                "apply_note": "scipy CSR (the reference's assembled, Dirichlet-eliminated operator) "
                              "times the k load-case fields, 1 thread; assembly not included",
                "sample": f"oracle (numpy/scipy restatement of the reference path) on {args.config}: "
