@@ -13,7 +13,7 @@ from .grid import Grid, level_set_h
 from .model import Compliance, Velocity
 
 
-def build(c, velocity=True):
+def build(c, velocity=True, direct=True):
     # tag 1 = clamp; one tag per distinct load patch (first-match tagging)
     rules, tags, seen = [(1, c.fixed)], [], {}
     for _, pred in c.loads:
@@ -30,7 +30,8 @@ def build(c, velocity=True):
         bf = fem.body_force_vector(space, c.body_force)
         loads = [v + bf for v in loads] if loads else [bf]
     model = Compliance(grid, c.lame, c.ersatz, clamp, loads, c.volume)
-    velocity = Velocity(grid, mass_weight=c.h1[0], stiffness_weight=c.h1[1]) if velocity else None
+    velocity = (Velocity(grid, mass_weight=c.h1[0], stiffness_weight=c.h1[1], direct=direct)
+                if velocity else None)
     phi0 = np.asarray(c.phi0(grid.vertices), dtype=float)
     params = Params(niter=c.niter, start_to_check=c.niter, reinit_step=c.reinit_step,
                     reinit_pars=c.reinit_pars)

@@ -351,7 +351,12 @@ class Velocity:
 
     def __init__(self, grid, mass_weight=1.0, stiffness_weight=1e-2,
                  boundary_normal_penalty=0.0, frozen_chi=None, frozen_penalty=0.0,
-                 zero_dirichlet=False):
+                 zero_dirichlet=False, direct=True):
+        # direct=False: Jacobi-CG to a 1e-14 relative residual instead of SuperLU
+        # (test-fixture generation on large 3D grids, where the LU fill of a 3D
+        # form is out of reach; the form is SPD and well conditioned, the two
+        # agree to ~1e-13, far inside every gate that uses theta)
+        self.direct = direct
         self.grid = grid
         self.space = fem.Space(grid, grid.dim)
         sp_ = self.space
@@ -369,7 +374,8 @@ class Velocity:
         if zero_dirichlet:
             self.bc = fem.clamp_dofs(sp_, np.arange(len(grid.boundary_facets)))
             solvable, _ = fem.dirichlet_eliminate(self.form_matrix, np.zeros(sp_.dof_count), self.bc)
-        self.lu = spla.splu(solvable.tocsc())
+        self.solvable = solvable.tocsr()
+        self.lu = spla.splu(solvable.tocsc()) if direct else None
 
     def _normal_matrix(self):
         grid, d = self.grid, self.grid.dim
@@ -393,8 +399,30 @@ class Velocity:
         if self.bc is not None:
             rhs = rhs.copy()
             rhs[self.bc] = 0.0
-        theta = self.lu.solve(rhs)
+        theta = self.lu.solve(rhs) if self.direct else _jacobi_cg(self.solvable, rhs, 1e-14)
         return theta, float(theta @ (self.form_matrix @ theta)), float(vec @ theta)
+
+
+def _jacobi_cg(A, b, rtol, maxiter=20000):
+    """Plain Jacobi-preconditioned CG (numpy), stopping at ||r|| <= rtol ||b||."""
+    dinv = 1.0 / A.diagonal()
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = dinv * r
+    p = z.copy()
+    rz = float(r @ z)
+    stop = rtol * float(np.linalg.norm(b))
+    for _ in range(maxiter):
+        if float(np.linalg.norm(r)) <= stop:
+            break
+        q = A @ p
+        alpha = rz / float(p @ q)
+        x += alpha * p
+        r -= alpha * q
+        z = dinv * r
+        rz, rz_old = float(r @ z), rz
+        p = z + (rz / rz_old) * p
+    return x
 
 
 @dataclass(frozen=True)

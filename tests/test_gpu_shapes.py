@@ -3,7 +3,9 @@
 The stencil kernels tile the lattice (2D: 30 owned columns per warp, 4 warps
 per CTA, row segments marched per CTA; 3D: 30 columns x 7 owned rows per CTA,
 z segments, cp.async staging of 16-byte row chunks with a separate path for
-the array's last row).  These shapes sit on and around every tile edge,
+the array's last row; 3D cubic elasticity: 31 columns x 7 owned rows per CTA,
+bulk-copy staging with a plain-load path for windows at either end of the
+array).  These shapes sit on and around every tile edge,
 include single-cell axes, and use a seeded random level set so every material
 count 0..nq occurs.  Gates as the north star: apply / diagonal / S1 vector /
 one level-set step <= 1e-10 (diagonal 1e-12), CG solutions <= 1e-8.
@@ -33,7 +35,8 @@ SHAPES_2D = [(1, 1), (1, 7), (2, 1), (29, 3), (30, 4), (31, 5), (60, 2), (61, 9)
 # (n, cubic): cubic grids take the symmetric-flux elasticity kernel (ElastC)
 SHAPES_3D = [((1, 1, 1), False), ((2, 1, 3), False), ((30, 7, 2), False), ((31, 8, 1), False),
              ((1, 13, 2), False), ((61, 14, 3), False), ((1, 1, 1), True), ((31, 8, 2), True),
-             ((30, 7, 9), True), ((3, 15, 4), True)]
+             ((30, 7, 9), True), ((3, 15, 4), True), ((32, 14, 5), True), ((62, 6, 13), True),
+             ((61, 15, 40), True)]
 
 
 def host(t):
