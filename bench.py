@@ -1,44 +1,63 @@
 #!/usr/bin/env python
 """Benchmark of the level-set compliance loop on B200 (see DESIGN.md section "Measurement").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config cfg5]
 
 One step = one optimisation iteration of the full loop (batched state PCG,
-compliance + shape derivative, H1 velocity solve, transport, reinit every 5)
-on BASELINE.json configs[1] (cfg2: 1024x256 bridge, 8 load cases).  Prints
-one JSON line on rank 0.  N > 1 runs N independent replicas (one per GPU,
-"replicas only": the north star is single-GPU; no collective on the data path).
+compliance + shape derivative, H1 velocity solve, transport, reinit every 5).
+The default workload is BASELINE.json configs[4] (cfg5: 192x96x96 Kuhn box,
+5.4M dofs, 4 load cases batched) -- the largest full-loop configuration on one
+GPU; cfg2 (the 2D bridge, configs[1]) is reported beside it as `secondary`.
+Prints one JSON line on rank 0.  N > 1 runs N independent replicas (one per
+GPU, "replicas only": the north star is single-GPU; no collective on the data
+path).
+
+`--impl reference` times the reference's CPU algorithm (the numpy/scipy oracle:
+the reference itself is Python and does not travel to the GPU box) on bounded
+samples of the same workload and extrapolates to whole iterations with the
+per-iteration counts the B200 arm measured in the same window
+(profiles/r02_calibration.json); the extrapolation is an explicit field and
+`ms_per_step` is the time each step really took.
 """
 
-import argparse
-import json
-import math
 import os
-import statistics
-import subprocess
-import sys
-import tempfile
-import threading
-import time
 
-import numpy as np
+# one BLAS thread per process for the CPU legs: the oracle's scipy cg is a chain of
+# small BLAS calls, which threaded OpenBLAS slows down ~50x on a shared host
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import tempfile  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "optimization iters/sec"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+CALIBRATION = os.path.join(ROOT, "profiles", "r02_calibration.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")
 FALLBACK_HBM = 6650.0
-# Mean state-PCG right-hand-side iterations per outer iteration of cfg2 over
-# the default window (iterations 3..12), measured by this bench on B200
-# (profiles/r01_bench_notes.md); used to extrapolate the bounded CPU sample to
-# a whole iteration.  Same algorithm and stopping rule on both sides.
-CFG2_RHS_ITERS_PER_OUTER = 127687.0
-# PCG right-hand-side iterations per outer iteration measured on the B200 runs
-# (tools/loop_profile.py; cfg4 = its one solve to 1e-8), used to extrapolate the
-# bounded CPU samples of the reference arm
-RHS_ITERS_PER_OUTER = {"cfg1": 2132.0, "cfg2": CFG2_RHS_ITERS_PER_OUTER, "cfg3": 2200.0,
-                       "cfg4": 197320.0, "cfg5": 17079.0}
+
+WORKLOAD = {
+    "cfg1": "cfg1: 2D cantilever 160x80 P1 (26,082 dofs), 1 load case",
+    "cfg2": "cfg2: 2D bridge 1024x256 P1 (526,850 dofs), 8 load cases batched",
+    "cfg3": "cfg3: 3D cantilever 96x48x48 Kuhn tets (698,691 dofs), 1 load case",
+    "cfg4": "cfg4: 2D stress test 4096x2048 P1 (16.8M dofs), body force, 1 load case",
+    "cfg5": "cfg5: 3D box 192x96x96 Kuhn tets (5,447,811 dofs), 4 load cases batched",
+}
+PCG_KERNELS = {2: "single-pass 2D PCG iteration march_pcg_rqs (r, z, p, x of iteration i and "
+                  "q_i = A p_i in one launch; q_{i-1} recomputed, not stored)",
+               3: "3D PCG iteration = pcg_prep (p = M^-1 r + beta p, pending x updates) + "
+                  "march3s<ElastC,PCGQ> (q = A p, p.q) + pcg_update (r -= alpha q, r.M^-1 r, r.r); "
+                  "a batch runs as two halves on two streams"}
 
 
 def parse():
@@ -47,9 +66,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the cfg2 loop beside the headline")
     ap.add_argument("--no-largest", action="store_true",
                     help="skip the apply measurements on the largest 2D / 3D meshes (cfg4, cfg5)")
     ap.add_argument("--shard-loads", action="store_true",
@@ -59,75 +79,6 @@ def parse():
     return ap.parse_args()
 
 
-def largest_applies(hbm, fp64_peak):
-    """The north star's apply gate on the largest meshes: cfg4 (2D, 4096x2048, k = 1) and
-    cfg5 (3D, 192x96x96 Kuhn tets, k = 4), random two-phase material, clamped x = 0,
-    L2 flushed (256 MB write + read) before each launch.  Bytes: 16 d k N + material."""
-    import torch
-
-    from paper_2601_05709_b200 import build_box_mesh, build_rect_mesh
-    from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace
-
-    out = {}
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    clean = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
-    for name, dim, n, k in (("cfg4", 2, (4096, 2048), 1), ("cfg5", 3, (192, 96, 96), 4)):
-        rule = [(1, lambda p: p[:, 0] < 1e-12)]
-        if dim == 2:
-            mesh = build_rect_mesh((0.0, 0.0, 2.0, 1.0), n[0], n[1], rule)
-            lame = (0.3 / 0.91, 1.0 / 2.6)
-        else:
-            mesh = build_box_mesh((0.0, 0.0, 0.0, 2.0, 1.0, 1.0), n, rule)
-            lame = (0.3 / (1.3 * 0.4), 1.0 / 2.6)
-        N, E = mesh.num_vertices, mesh.num_elements
-        space = FunctionSpace(mesh, dim)
-        phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
-        op = ElasticityOperator(space, phi, lame, 1e-3, DirichletSet.on_tags(space, 1))
-        u = torch.randn((k, dim * N), dtype=torch.float64, device="cuda")
-        op.apply(u)
-        torch.cuda.synchronize()
-        torch.cuda._sleep(100_000_000)
-        evs = []
-        for rep in range(13):
-            flush.fill_(float(rep))
-            clean.sum()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            op.apply(u)
-            a1.record(stream)
-            if rep >= 3:
-                evs.append((a0, a1))
-        torch.cuda.synchronize()
-        t = statistics.median([e0.elapsed_time(e1) / 1e3 for e0, e1 in evs])
-        byts = 16.0 * dim * k * N + (E if dim == 2 else 4.0 * N)
-        out[name] = {"grid": "x".join(map(str, n)), "k": k, "ms": t * 1e3,
-                     "dof_per_s": k * dim * N / t, "gbs": byts / t / 1e9,
-                     "frac": byts / t / 1e9 / hbm, "bytes": byts}
-        del op, u
-    # Kuhn-tet stencil: ~220 fp64 instructions per cell and field (DESIGN.md section 3)
-    cells = 192 * 96 * 96
-    lanes = 220.0 * cells * 4
-    t_fp64 = lanes / ((fp64_peak or 34.172e12) / 2)  # DFMA lane-ops/s = FLOP/s / 2
-    out["cfg5"]["fp64_bound_ms"] = t_fp64 * 1e3
-    out["cfg5"]["fp64_pipe_frac"] = t_fp64 / (out["cfg5"]["ms"] / 1e3)
-    out["cfg5"]["note"] = ("fp64-issue-bound: ~220 fp64 instructions per cell and field need %.0f us "
-                           "at the measured fp64 peak, which caps the HBM fraction near 0.6 even at "
-                           "100%% of the fp64 pipe; fp64_pipe_frac is this op count over the "
-                           "measured time" % (t_fp64 * 1e6))
-    del flush, clean
-    return out
-
-
-def ncu_traffic():
-    """DRAM bytes per fused PCG iteration from the committed ncu --set full capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_pcg_rq.json")) as f:
-            return float(json.load(f)["traffic_bytes_per_pcg_iteration"])
-    except Exception:
-        return None
-
-
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -135,6 +86,15 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return FALLBACK_HBM, "fallback"
+
+
+def ncu_kernels():
+    """Committed ncu --set full counters per kernel (profiles/r02_ncu_kernels.json)."""
+    try:
+        with open(NCU_SUMMARY) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 class ClockSampler:
@@ -196,114 +156,220 @@ def dist_info():
 
 
 # ---------------------------------------------------------------------------------------------
-# CPU baseline: the oracle (numpy/scipy restatement of the reference path) on a bounded sample
+# CPU side: the oracle (numpy/scipy restatement of the reference path) on bounded samples
 # ---------------------------------------------------------------------------------------------
 
-def cpu_sample(c, cg_iters_per_load, threads):
-    """Time one bounded outer iteration of the oracle on config c.
+_SYS = None
 
-    Measured: assembly + Dirichlet elimination of the shared operator (all
-    loads), ``cg_iters_per_load`` Jacobi-PCG iterations per load (scipy cg, as
-    the reference, fem.py:306; loads on ``threads`` threads like the
-    reference's task_parallel mode, driver.py:185), the S1 tensor + derivative
-    vector, and one transport call of the explicit scheme.  Not measured (so
-    the CPU figure is optimistic): the velocity form's one-time SuperLU
-    factorisation and per-iteration triangular solves, and reinitialisation.
-    Returns dict of seconds.
-    """
-    from concurrent.futures import ThreadPoolExecutor
 
-    from oracle import cases as ocases, fem as ofem, levelset as olevel, model as omodel
+def _cg_sample(args):
+    """Seconds per scipy-cg iteration, setup excluded (difference of two runs of n and
+    2n iterations, n grown until the longer run takes >= 0.2 s)."""
+    from oracle import fem as ofem
+    A, b, iters = _SYS
 
-    grid, model, _, phi, _, h = ocases.build(c, velocity=False)
-    t0 = time.perf_counter()
-    systems = model.eliminated(phi)
-    t_asm = time.perf_counter() - t0
-
-    def one(args):
-        A, b = args
+    def run(n):
+        t0 = time.perf_counter()
         try:
-            ofem.jacobi_pcg(A, b, maxiter=cg_iters_per_load)
+            ofem.jacobi_pcg(A, b, rtol=0.0, atol=0.0, maxiter=n)
         except ofem.SolverError:
             pass
+        return time.perf_counter() - t0
 
+    n = iters
+    while True:
+        t1, t2 = run(n), run(2 * n)
+        if t2 >= 0.2 or n >= 4096:
+            return max(t2 - t1, 1e-9) / n
+        n *= 4
+
+
+def cpu_units(c, procs, slab=None, cg_iters=6, vel_iters=6):
+    """Per-unit costs of one outer iteration of the reference's CPU algorithm on config c.
+
+    Measured on a slab of the config's own mesh (same cell size; full x-y
+    extent, `slab` cells along the last axis) and scaled by the element ratio:
+    every oracle operation here is a sweep over elements or CSR rows, linear in
+    the mesh size.  Units: assembly + Dirichlet elimination of the shared
+    operator for all loads (reference fem.py:141-150,274-291, once per
+    iteration), one scipy-cg Jacobi-PCG iteration per right-hand side
+    (fem.py:294-316; `procs` right-hand sides run concurrently in forked
+    processes, the most the reference's task-parallel mode could use), S1 +
+    derivative vector (compliance.py:128-139, velocity.py:129-142), one CG
+    iteration of the H1 velocity form (3D; velocity.py:98-154 factors it with
+    SuperLU, out of reach at 3D sizes), one transport substep and one reinit
+    substep of the explicit scheme (the north star's level-set update)."""
+    import multiprocessing as mp
+
+    from oracle import cases as ocases, levelset as olevel, model as omodel
+
+    global _SYS
+    n = tuple(c.n)
+    full_cells = float(np.prod(n))
+    if slab is None:
+        slab = max(1, int(round(n[-1] / 32))) if c.dim == 3 else max(2, int(round(n[-1] / 16)))
+    slab = min(slab, n[-1])
+    h_last = (c.hi[-1] - c.lo[-1]) / n[-1]
+    # slab of the mesh; clamp on x = lo and the k load cases on the x = hi face, so that
+    # every slab has both (the timed costs do not depend on where the patches sit)
+    x0, x1 = c.lo[0], c.hi[0]
+    patch = (lambda p: p[:, 0] > x1 - 1e-12)
+    sc = type(c)(**{**c.__dict__, "n": n[:-1] + (slab,),
+                    "hi": tuple(c.hi[:-1]) + (c.lo[-1] + slab * h_last,),
+                    "fixed": (lambda p: p[:, 0] < x0 + 1e-12),
+                    "loads": tuple((g, patch) for g, _ in c.loads)})
+    scale = full_cells / float(np.prod(sc.n))
+    grid, model, _, phi, _, h = ocases.build(sc, velocity=False)
+    rng = np.random.default_rng(0)
+    out = {"slab": "x".join(map(str, sc.n)), "scale": scale}
     t0 = time.perf_counter()
-    if threads > 1:
-        with ThreadPoolExecutor(max_workers=threads) as pool:
-            list(pool.map(one, systems))
+    systems = model.eliminated(phi)
+    out["assembly_s"] = (time.perf_counter() - t0) * scale
+    A = systems[0][0]
+    p = max(1, min(procs, len(systems)))
+    _SYS = (A, rng.standard_normal(A.shape[0]), cg_iters)
+    if p > 1:  # concurrent right-hand sides; each worker times its own iterations
+        with mp.get_context("fork").Pool(p) as pool:
+            wall = max(pool.map(_cg_sample, range(p)))
     else:
-        for s in systems:
-            one(s)
-    t_cg = time.perf_counter() - t0
-    states = [np.sin(np.arange(model.space.dof_count) * (1e-3 * (k + 1))) * 1e-3
-              for k in range(len(systems))]
+        wall = _cg_sample(0)
+    _SYS = None
+    out["pcg_rhs_iter_s"] = wall / p * scale
+    out["pcg_procs"] = p
+    states = [rng.standard_normal(model.space.dof_count) * 1e-3 for _ in systems]
     t0 = time.perf_counter()
     s1 = model.s1_combined(phi, states, 0.5)
     vec = omodel.derivative_vector(model.space, s1=s1)
-    t_s1 = time.perf_counter() - t0
+    out["s1_rhs_s"] = (time.perf_counter() - t0) * scale
+    vel = omodel.Velocity(grid, mass_weight=c.h1[0], stiffness_weight=c.h1[1], direct=False)
+    B = vel.solvable
+    m = vel_iters
+    while True:
+        tv = []
+        for mm in (m, 2 * m):
+            t0 = time.perf_counter()
+            omodel._jacobi_cg(B, -vec, 0.0, maxiter=mm)
+            tv.append(time.perf_counter() - t0)
+        if tv[1] >= 0.2 or m >= 4096:
+            break
+        m *= 4
+    vel_iters = m
+    out["velocity_iter_s"] = max(tv[1] - tv[0], 1e-9) / vel_iters * scale
     theta = -vec / (np.abs(vec).max() + 1e-30)
     t0 = time.perf_counter()
-    _, nsub = olevel.transport(grid, phi, theta, 1e-3, 8, False, h)
-    t_tr = time.perf_counter() - t0
-    # the reference's apply: its assembled, eliminated CSR operator times the k fields
-    A = systems[0][0]
-    U = np.random.default_rng(0).standard_normal((A.shape[0], len(systems)))
-    A @ U
+    _, nsub = olevel.transport(grid, phi, theta, 1e-9, 2, False, h)
+    out["transport_substep_s"] = (time.perf_counter() - t0) / nsub * scale
     t0 = time.perf_counter()
-    for _ in range(5):
-        A @ U
-    t_apply = (time.perf_counter() - t0) / 5
-    return {"asm": t_asm, "cg": t_cg, "cg_rhs_iters": cg_iters_per_load * len(systems),
-            "s1": t_s1, "transport": t_tr, "k": len(systems), "n": model.space.dof_count,
-            "apply": t_apply}
+    _, nr = olevel.reinitialize(grid, phi, 2, 1e-9, h)
+    out["reinit_substep_s"] = (time.perf_counter() - t0) / nr * scale
+    return out
 
 
-def cpu_iters_per_sec(s, rhs_iters_per_outer):
-    per_rhs_iter = s["cg"] / s["cg_rhs_iters"]
-    t_outer = s["asm"] + per_rhs_iter * rhs_iters_per_outer + s["s1"] + s["transport"]
-    return 1.0 / t_outer, t_outer
+def cpu_seconds_per_iteration(u, counts):
+    """Extrapolate the per-unit costs to one outer iteration with measured counts."""
+    return (u["assembly_s"] + u["pcg_rhs_iter_s"] * counts["rhs_pcg_iters"] + u["s1_rhs_s"]
+            + u["velocity_iter_s"] * counts["velocity_iters"]
+            + u["transport_substep_s"] * counts["transport_substeps"]
+            + u["reinit_substep_s"] * counts["reinit_substeps"])
+
+
+def window_counts(recs):
+    n = max(len(recs), 1)
+    return {"rhs_pcg_iters": sum(sum(r.cg_iters) for r in recs) / n,
+            "velocity_iters": sum(r.velocity_iters for r in recs) / n,
+            "transport_substeps": sum(r.transport_substeps for r in recs) / n,
+            "reinit_substeps": sum(r.reinit_substeps for r in recs) / n}
 
 
 # ---------------------------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------------------------
 
-def b200_arm(args, world, rank, local):
+def flushed_apply_ms(op, u, reps=13):
+    """Median standalone apply time, L2 flushed (256 MB write + 256 MB read of another
+    buffer, so the flush's dirty lines are written back before the timed launch)."""
     import torch
-    import torch.distributed as dist
 
-    import paper_2601_05709_b200 as lsg
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    clean = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    op.apply(u)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(100_000_000)  # events bracket device time, not host launches
+    evs = []
+    for rep in range(reps):
+        flush.fill_(float(rep))
+        clean.sum()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        op.apply(u)
+        a1.record(stream)
+        if rep >= 3:
+            evs.append((a0, a1))
+    torch.cuda.synchronize()
+    del flush, clean
+    return statistics.median([e0.elapsed_time(e1) for e0, e1 in evs])
+
+
+def largest_applies(hbm, ncu):
+    """The north star's apply gate on the largest meshes: cfg4 (2D, 4096x2048, k = 1) and
+    cfg5 (3D, 192x96x96 Kuhn tets, k = 4), random two-phase material, clamped x = 0.
+    Bytes: 16 d k N + E (material 1 B per element)."""
+    import torch
+
+    from paper_2601_05709_b200 import build_box_mesh, build_rect_mesh
+    from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace
+
+    out = {}
+    for name, dim, n, k in (("cfg4", 2, (4096, 2048), 1), ("cfg5", 3, (192, 96, 96), 4)):
+        rule = [(1, lambda p: p[:, 0] < 1e-12)]
+        if dim == 2:
+            mesh = build_rect_mesh((0.0, 0.0, 2.0, 1.0), n[0], n[1], rule)
+            lame = (0.3 / 0.91, 1.0 / 2.6)
+        else:
+            mesh = build_box_mesh((0.0, 0.0, 0.0, 2.0, 1.0, 1.0), n, rule)
+            lame = (0.3 / (1.3 * 0.4), 1.0 / 2.6)
+        N, E = mesh.num_vertices, mesh.num_elements
+        space = FunctionSpace(mesh, dim)
+        phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
+        op = ElasticityOperator(space, phi, lame, 1e-3, DirichletSet.on_tags(space, 1))
+        u = torch.randn((k, dim * N), dtype=torch.float64, device="cuda")
+        ms = flushed_apply_ms(op, u)
+        byts = 16.0 * dim * k * N + E
+        kern = ncu.get(f"apply_{name}", {})
+        out[name] = {"grid": "x".join(map(str, n)), "k": k, "ms": ms, "dof_per_s": k * dim * N / (ms / 1e3),
+                     "gbs": byts / (ms / 1e3) / 1e9, "frac": byts / (ms / 1e3) / 1e9 / hbm, "bytes": byts,
+                     "ncu": kern or None}
+        del op, u
+    return out
+
+
+def loop_window(c, W, K, world, sharded, dist):
+    """W untimed + K device-timed optimisation iterations; returns the timing record."""
+    import torch
+
     from paper_2601_05709_b200 import _lib, configs, fem
     from paper_2601_05709_b200.driver import Optimizer
 
-    torch.cuda.set_device(local)
     lib = _lib.load()
-    c = configs.case(args.config)
-    W, K = args.warmup, args.steps
     c = type(c)(**{**c.__dict__, "niter": W + K})
     mesh, model, phi, params = configs.build(c)
-    sharded = bool(args.shard_loads and world > 1)
     if sharded:
         from paper_2601_05709_b200.parallel import ShardedCompliance
         model = ShardedCompliance(model)
-    d, N, E = mesh.dim, mesh.num_vertices, mesh.num_elements
-    k = int(model.load_vectors.shape[0])
+    opt = Optimizer(model, phi, params, timing=False)
+    for _ in range(W):
+        opt.step()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # ---- device-resident loop: W warm-up + K timed optimisation iterations ----------------
-    opt = Optimizer(model, phi, params, timing=False)
-    for _ in range(W):
-        opt.step()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     fem.PCG_PROFILE = []
     launches0 = lib.lsg_launch_count()
-    clocks = ClockSampler(local)
-    clocks.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -312,77 +378,98 @@ def b200_arm(args, world, rank, local):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    clk = clocks.stop()
     launches = lib.lsg_launch_count() - launches0
     prof, fem.PCG_PROFILE = fem.PCG_PROFILE, None
     t_local = e0.elapsed_time(e1) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
-    value = (1 if sharded else world) * K / t_max
+    return {"mesh": mesh, "model": opt.model, "opt": opt, "recs": recs, "prof": prof,
+            "t_local": t_local, "t_max": float(t.item()), "launches": int(launches)}
 
-    # ---- roofline of the dominant kernel pair: the fused PCG iteration ----------------
-    # (80 k + 16) d N + E bytes per iteration of k right-hand sides.
-    state_chunks = [p for p in prof if p["kind"] == _lib.LSG_OP_ELASTICITY]
-    pcg_ms = sum(p["events"][0].elapsed_time(p["events"][1]) for p in state_chunks)
-    rhs_iters = sum(p["rhs_iters"] for p in state_chunks)
-    launched_iters = sum(p["launched"] for p in state_chunks)
-    max_iters = sum(p["max_iters"] for p in state_chunks)
+
+def pcg_roofline(lw, hbm, peak_kind, ncu):
+    from paper_2601_05709_b200 import _lib
+
+    mesh = lw["mesh"]
+    d, N, E = mesh.dim, mesh.num_vertices, mesh.num_elements
+    prof = lw["prof"]
+    state = [p for p in prof if p["kind"] == _lib.LSG_OP_ELASTICITY]
+    pcg_ms = sum(p["events"][0].elapsed_time(p["events"][1]) for p in state)
+    rhs_iters = sum(p["rhs_iters"] for p in state)
+    launched = sum(p["launched"] for p in state)
+    max_iters = sum(p["max_iters"] for p in state)
+    # (80 k + 16) d N + E bytes per iteration of k right-hand sides
+    # = 80 d N per right-hand-side iteration + (16 d N + E) per batched iteration
     pcg_bytes = 80.0 * d * N * rhs_iters + (16.0 * d * N + E) * max_iters
-    hbm, peak_kind = peaks()
     achieved = pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms > 0 else 0.0
     all_ms = sum(p["events"][0].elapsed_time(p["events"][1]) for p in prof)
+    key = f"pcg{d}d"
+    kern = ncu.get(key, {})
+    traffic = kern.get("dram_bytes_per_iteration")
+    return {"bound": "hbm", "kernel": PCG_KERNELS[d], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+            "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration (canonical two-pass)",
+            "us_per_batched_iteration": pcg_ms * 1e3 / max(max_iters, 1),
+            "pcg_ms_in_timed_region": pcg_ms, "pcg_share_of_step": all_ms / (lw["t_local"] * 1e3),
+            "rhs_iterations": rhs_iters, "batched_iterations": max_iters, "launched_iterations": launched,
+            "ncu": kern or None,
+            "traffic_note": "DRAM bytes per batched PCG iteration (all its launches) from the committed "
+                            "ncu --set full capture (profiles/r02_ncu_kernels.json, cold cache)"}
 
-    # ---- standalone elasticity apply (k = 8), L2 flushed between launches ------------------
-    # Flush = a 256 MB write (evicts every line the apply touched), then a 256 MB read of
-    # another buffer so that the flush's dirty lines are written back before the timed
-    # launch instead of inside it.  Both runs are reported; `ms` is the clean-flush one.
-    op = opt.model.operator(opt.phi)
+
+def b200_arm(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_05709_b200 as lsg
+    from paper_2601_05709_b200 import configs
+
+    torch.cuda.set_device(local)
+    c = configs.case(args.config)
+    W, K = args.warmup, args.steps
+    sharded = bool(args.shard_loads and world > 1)
+    hbm, peak_kind = peaks()
+    ncu = ncu_kernels()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    lw = loop_window(c, W, K, world, sharded, dist)
+    clk = clocks.stop()
+    mesh, model, recs = lw["mesh"], lw["model"], lw["recs"]
+    d, N, E = mesh.dim, mesh.num_vertices, mesh.num_elements
+    k = int(model.load_vectors.shape[0])
+    t_max = lw["t_max"]
+    value = (1 if sharded else world) * K / t_max
+    roof = pcg_roofline(lw, hbm, peak_kind, ncu)
+    counts = window_counts(recs)
+    launches = lw["launches"]
+
+    # ---- standalone apply of this config's operator (k RHS), L2 flushed ------------------
+    op = lw["opt"].model.operator(lw["opt"].phi)
     u = torch.randn((k, d * N), dtype=torch.float64, device="cuda")
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    clean = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-
-    def apply_times(clean_flush):
-        # queued behind a device sleep: the events bracket device time, not the host launch
-        torch.cuda.synchronize()
-        torch.cuda._sleep(100_000_000)
-        evs = []
-        for rep in range(23):
-            flush.fill_(float(rep))
-            if clean_flush:
-                clean.sum()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            op.apply(u)
-            a1.record(stream)
-            if rep >= 3:
-                evs.append((a0, a1))
-        torch.cuda.synchronize()
-        return statistics.median([e0.elapsed_time(e1) / 1e3 for e0, e1 in evs])
-
-    t_apply_dirty = apply_times(False)
-    t_apply = apply_times(True)
-    del flush, clean
+    ms = flushed_apply_ms(op, u)
     apply_bytes = 16.0 * d * k * N + E
+    apply = {"k": k, "ms": ms, "dof_per_s": k * d * N / (ms / 1e3), "gbs": apply_bytes / (ms / 1e3) / 1e9,
+             "frac": apply_bytes / (ms / 1e3) / 1e9 / hbm, "bytes": apply_bytes,
+             "flush": "256 MB write + 256 MB read of another buffer before each launch"}
+    del op, u
+    del lw
 
     largest = None
     if not args.no_largest and rank == 0:
-        fp64 = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
-                fp64 = float(json.load(f)["fp64_tflops"]) * 1e12
-        except Exception:
-            fp64 = None
-        largest = largest_applies(hbm, fp64)
+        largest = largest_applies(hbm, ncu)
 
-    # ---- end to end through the public API from host buffers ----------------------------
+    # ---- end to end: the config's own run through the public run() from host buffers ------
     e2e = None
     if not args.no_e2e:
         torch.cuda.synchronize()
-        barrier()
-        phi_host = torch.from_numpy(np.ascontiguousarray(c.phi0(mesh.vertices), dtype=np.float64)).pin_memory()
-        loads_host = model.load_vectors.cpu().pin_memory()
+        if world > 1:
+            dist.barrier()
+        m0 = configs.build(c)[0]
+        phi_host = torch.from_numpy(np.ascontiguousarray(c.phi0(m0.vertices if c.name != "cfg4" else None),
+                                                         dtype=np.float64)).pin_memory()
+        del m0
         out_host = torch.empty(N, dtype=torch.float64).pin_memory()
         d2h = [0]
 
@@ -392,43 +479,57 @@ def b200_arm(args, world, rank, local):
 
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        m2, model2, _, params2 = configs.build(c)          # loads assembled host-side, uploaded
-        model2._loads.copy_(loads_host, non_blocking=True)  # explicit pinned H2D of the loads
+        m2, model2, _, params2 = configs.build(c)             # loads assembled host-side, uploaded
+        loads_host = model2.load_vectors.cpu().pin_memory()
+        model2._loads.copy_(loads_host, non_blocking=True)    # explicit pinned H2D of the loads
         phi_dev = lsg.LevelSetField.from_field(
             lsg.FemField(lsg.FunctionSpace(m2, 1), phi_host.to("cuda", non_blocking=True)))
-        lsg.run(model2, phi_dev, params2, on_record=on_record, timing=False)
+        _, hist = lsg.run(model2, phi_dev, params2, on_record=on_record, timing=False)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
         te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        n_it = W + K
+        n_it = len(hist)
         h2d = (phi_host.numel() + loads_host.numel()) * 8
         e2e = {"value": world * n_it / float(te.item()), "unit": "iters/s",
                "h2d_bytes_per_step": int(h2d / n_it), "d2h_bytes_per_step": int(d2h[0] / n_it),
-               "iterations": n_it,
-               "note": "public run() from pinned host phi0/loads, niter=W+K incl. the cold-start "
-                       "first iterations; phi + record read back to host every iteration"}
+               "iterations": n_it, "time_to_solution_s": float(te.item()),
+               "final": {"J": hist[-1].cost, "C": float(hist[-1].constraint[0])},
+               "note": f"time to solution: the config's own {n_it}-iteration run through the public "
+                       "run() from pinned host phi0 / loads (cold start, mesh + model setup included), "
+                       "phi + record read back to the host every iteration"}
+        del model2, phi_dev
+
+    # ---- secondary: the 2D bridge loop (BASELINE configs[1]) --------------------------------
+    secondary = None
+    if not args.no_secondary and args.config != "cfg2" and rank == 0 and world == 1:
+        c2 = configs.case("cfg2")
+        lw2 = loop_window(c2, 3, 10, 1, False, dist)
+        roof2 = pcg_roofline(lw2, hbm, peak_kind, ncu)
+        secondary = {"config": WORKLOAD["cfg2"], "window": "warmup 3, 10 timed iterations",
+                     "value": 10 / lw2["t_max"], "unit": "iters/s",
+                     "pcg_us_per_iteration": roof2["us_per_batched_iteration"],
+                     "pcg_frac": roof2["frac"], "pcg_share_of_step": roof2["pcg_share_of_step"],
+                     "rhs_pcg_iters_per_outer": window_counts(lw2["recs"])["rhs_pcg_iters"]}
+        del lw2
 
     # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------------
     cpu = None
-    rhs_per_outer = sum(sum(r.cg_iters) for r in recs) / K
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        s = cpu_sample(c, cg_iters_per_load=25, threads=1)
-        v, t_outer = cpu_iters_per_sec(s, rhs_per_outer)
-        cpu = {"value": v, "unit": "iters/s", "cores": 1, "kind": "port",
-               "apply_dof_per_s": s["k"] * s["n"] / s["apply"],
-               "breakdown": {"assembly_s": s["asm"], "pcg_ms_per_rhs_iteration": s["cg"] / s["cg_rhs_iters"] * 1e3,
-                             "s1_and_rhs_s": s["s1"], "transport_s": s["transport"]},
-               "apply_note": "scipy CSR (the reference's assembled, Dirichlet-eliminated operator) "
-                             "times the k load-case fields, 1 thread; assembly not included",
-               "sample": f"oracle (numpy/scipy restatement of the reference path) on {args.config}: "
-                         f"assembly+elimination, 25 scipy-cg Jacobi-PCG iterations x {s['k']} loads, "
-                         f"S1 + derivative vector, one transport; extrapolated to "
-                         f"{rhs_per_outer:.0f} PCG rhs-iterations/outer iteration measured here; "
-                         f"velocity LU + reinit not counted (CPU figure optimistic); "
-                         f"{s['cg'] / s['cg_rhs_iters'] * 1e3:.2f} ms per PCG rhs-iteration, "
-                         f"{t_outer:.1f} s per outer iteration"}
+        t0 = time.perf_counter()
+        units = cpu_units(c, procs=1)
+        t_sample = time.perf_counter() - t0
+        s_it = cpu_seconds_per_iteration(units, counts)
+        cpu = {"value": 1.0 / s_it, "unit": "iters/s", "cores": 1, "kind": "port",
+               "extrapolated_s_per_iteration": s_it, "units": units, "counts": counts,
+               "apply_dof_per_s": None,
+               "sample": f"oracle (numpy/scipy restatement of the reference path) on a {units['slab']} "
+                         f"slab of {args.config} (x{units['scale']:.0f} to the full mesh), 1 core, "
+                         f"{t_sample:.1f} s of CPU work: assembly + elimination, scipy-cg Jacobi-PCG "
+                         "iterations, S1 + derivative vector, H1 velocity CG iterations, transport and "
+                         "reinit substeps; extrapolated to one outer iteration with the counts this "
+                         "run's timed window measured"}
 
     if rank == 0:
         line = {
@@ -436,78 +537,86 @@ def b200_arm(args, world, rank, local):
             "warmup": W, "ms_per_step": 1e3 * t_max / K, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: 2D bridge 1024x256 P1 (526,850 dofs), 8 load "
-                                   "cases batched, full loop (state PCG rtol 1e-10, S1+RHS, H1 CG, "
-                                   "transport, reinit every 5)",
+            "config": {"workload": f"{WORKLOAD[args.config]}, full loop (state PCG rtol 1e-10, S1+RHS, "
+                                   f"H1 CG, transport, reinit every {c.reinit_step})",
+                       "window": f"iterations {W}..{W + K - 1} of the run (after {W} untimed warm-up "
+                                 "iterations); the PCG work per iteration depends on the window",
                        "nodes": N, "elements": E, "load_cases": k,
-                       "l2": "PCG working set (x,r,p,q for 8 rhs = 135 MB) exceeds the 126 MB L2; "
-                             "standalone apply timings flush L2 with a 256 MB write (+ a 256 MB "
-                             "read that cleans it) before each launch",
+                       "l2": "PCG working set exceeds the 126 MB L2 (cfg5: ~1.4 GB); standalone apply "
+                             "timings flush L2 before each launch",
                        "parallelism": (f"load cases sharded over {world} GPUs" if sharded else
                                        f"replicas x{world}" if world > 1 else "single GPU")},
-            "roofline": {"bound": "hbm", "kernel": "single-pass PCG iteration march_pcg_rqs "
-                                                   "(r, z, p, x of iteration i and q_i = A p_i in one "
-                                                   "launch; q_{i-1} = A p_{i-1} recomputed, not stored)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(),
-                         "traffic_note": "DRAM bytes of one PCG iteration (one launch) from "
-                                         "profiles/r01_ncu_pcg_rq.json (cold cache): below the "
-                                         "algorithmic (canonical two-pass, 10 vectors per rhs) "
-                                         "count because the pass moves 6 vectors per rhs (q is "
-                                         "recomputed, x updated in the same pass) and some writes "
-                                         "stay in L2; achieved/peak is the canonical-byte rate, the "
-                                         "actual DRAM rate is traffic / launch time",
-                         "peak_kind": peak_kind,
-                         "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration",
-                         "pcg_ms_in_timed_region": pcg_ms, "pcg_share_of_step": all_ms / (t_local * 1e3),
-                         "rhs_iterations": rhs_iters, "launched_iterations": launched_iters},
-            "apply": {"k": k, "ms": t_apply * 1e3, "dof_per_s": k * d * N / t_apply,
-                      "gbs": apply_bytes / t_apply / 1e9, "frac": apply_bytes / t_apply / 1e9 / hbm,
-                      "bytes": apply_bytes, "ms_dirty_flush": t_apply_dirty * 1e3,
-                      "flush": "256 MB write + 256 MB read of another buffer before each launch "
-                               "(ms_dirty_flush: write only; the flush's dirty lines are then "
-                               "written back during the timed launch)"},
+            "roofline": roof,
+            "apply": apply,
             "apply_largest": largest,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(launches),
+            "secondary": secondary,
+            "gpu_launches": launches,
             "clocks": clk,
             "history": {"J": [r.cost for r in recs], "C": [float(r.constraint[0]) for r in recs],
-                        "rhs_pcg_iters_per_outer": rhs_per_outer,
+                        "counts_per_outer": counts,
+                        "cg_iters": [list(r.cg_iters) for r in recs],
                         "velocity_iters": [r.velocity_iters for r in recs]},
         }
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------------------------
+# Reference arm: the reference's CPU algorithm (the oracle port) on the host cores
+# ---------------------------------------------------------------------------------------------
+
 def reference_arm(args, world, rank, local):
-    """The reference path on the host: the oracle port (numpy/scipy restatement of
-    lsopt's algorithm; the reference is Python and does not travel to the GPU box).
-    Each step is a bounded sample of one cfg2 outer iteration, extrapolated."""
+    """Each step: one bounded sample of the workload (per-unit costs on a slab of the
+    config's mesh), extrapolated to one outer iteration with the per-iteration counts
+    the B200 arm measured in the same window (profiles/r02_calibration.json)."""
     if rank != 0:
         return
     from paper_2601_05709_b200 import configs
 
     c = configs.case(args.config)
-    threads = min(8, os.cpu_count() or 1)
-    vals = []
+    procs = min(os.cpu_count() or 1, 8)
+    cal = None
+    try:
+        with open(CALIBRATION) as f:
+            cal_all = json.load(f)
+        window = f"w{args.warmup}k{args.steps}"
+        entry = cal_all.get(args.config, {})
+        cal = entry.get(window) or (entry[sorted(entry)[0]] if entry else None)
+        cal_window = window if window in entry else (sorted(entry)[0] if entry else None)
+    except Exception:
+        cal_window = None
+    if cal is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"no calibration for {args.config} in "
+                                                              "profiles/r02_calibration.json"}))
+        return
+    per_step, samples = [], []
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(c, cg_iters_per_load=10, threads=threads)
-        v, t_outer = cpu_iters_per_sec(s, RHS_ITERS_PER_OUTER[args.config])
+        t0 = time.perf_counter()
+        units = cpu_units(c, procs=procs)
+        dt = time.perf_counter() - t0
         if i >= args.warmup:
-            vals.append(t_outer)
-    t_outer = statistics.median(vals)
-    v = 1.0 / t_outer
+            per_step.append(dt)
+            samples.append(cpu_seconds_per_iteration(units, cal))
+    s_it = statistics.median(samples)
+    v = 1.0 / s_it
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_outer * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(per_step),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config} (same as the b200 arm)"},
-        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": "per step: oracle assembly + 10 scipy-cg PCG iterations per load "
-                                   f"({threads} threads, reference task_parallel mode) + S1/RHS + "
-                                   f"transport, extrapolated with {RHS_ITERS_PER_OUTER[args.config]:.0f} "
-                                   "PCG rhs-iterations per outer iteration"},
+        "config": {"workload": f"{WORKLOAD[args.config]} (same as the b200 arm)"},
+        "extrapolation": {"s_per_outer_iteration": s_it, "counts_per_outer": cal,
+                          "counts_window": cal_window, "units_last_step": units,
+                          "note": "value = 1 / s_per_outer_iteration; each step measured the per-unit "
+                                  "costs on a slab and extrapolated; ms_per_step is the step's real "
+                                  "duration"},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": procs, "kind": "port",
+                         "sample": f"per step: oracle (numpy/scipy restatement of the reference) on a "
+                                   f"{units['slab']} slab of {args.config}, scaled x{units['scale']:.0f}: "
+                                   f"assembly + elimination, scipy-cg PCG iterations ({units['pcg_procs']} "
+                                   "load cases in parallel processes), S1 + derivative vector, H1 velocity "
+                                   "CG iterations, transport + reinit substeps"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

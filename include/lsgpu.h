@@ -147,6 +147,11 @@ typedef struct {
 } lsg_pcg_ws;
 
 int32_t lsg_abi_version(void);
+/* sizeof of the ABI structs as compiled into the library: bindings assert
+ * their mirrors against these (lsg_op is 160 bytes: it ends in aux[4]). */
+int64_t lsg_sizeof_op(void);
+int64_t lsg_sizeof_pcg_ws(void);
+int64_t lsg_sizeof_grid(void);
 const char *lsg_last_error(void);
 /* Number of kernels this library has launched in the process so far. */
 int64_t lsg_launch_count(void);

@@ -65,6 +65,9 @@ _W = ctypes.POINTER(PcgWs)
 # symbol -> (restype, argtypes); the full export list of include/lsgpu.h
 SIGNATURES = {
     "lsg_abi_version": (ctypes.c_int32, []),
+    "lsg_sizeof_op": (ctypes.c_int64, []),
+    "lsg_sizeof_pcg_ws": (ctypes.c_int64, []),
+    "lsg_sizeof_grid": (ctypes.c_int64, []),
     "lsg_last_error": (ctypes.c_char_p, []),
     "lsg_launch_count": (ctypes.c_int64, []),
     "lsg_num_nodes": (ctypes.c_int64, [_G]),
@@ -118,6 +121,11 @@ def load(require_device=True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        for name, struct in (("lsg_sizeof_op", Op), ("lsg_sizeof_grid", Grid),
+                             ("lsg_sizeof_pcg_ws", PcgWs)):
+            if getattr(lib, name)() != ctypes.sizeof(struct):
+                raise NativeUnavailable(f"{LIB_PATH}: {name} = {getattr(lib, name)()} but the "
+                                        f"ctypes mirror has {ctypes.sizeof(struct)} bytes")
         _lib = lib
     return _lib
 

@@ -202,19 +202,35 @@ int lsg_inv_diag(const lsg_op *op, double *dinv, void *stream) {
   return DISPATCH(op->grid, inv_diag(*op, dinv, S(stream)), inv_diag(*op, dinv, S(stream)));
 }
 
-static int check_ws(const lsg_pcg_ws *ws) {
+// The buffers each path reads unconditionally must be present: 2D forms r_i
+// into r_alt and keeps q_alt for the stored-q / persistent passes; 3D rotates
+// three direction buffers (p, p_alt, p_ring).  A missing one is an argument
+// error, not an illegal address that poisons the context.
+static int check_ws(const lsg_op *op, const lsg_pcg_ws *ws) {
   if (!ws || ws->k < 1 || ws->k > 65535 || !ws->x || !ws->b || !ws->r || !ws->p || !ws->q ||
       !ws->scal || !ws->partials || !ws->counters || !ws->p_alt || !ws->dinv) {
     set_error("incomplete PCG workspace");
     return LSG_ERR_ARG;
   }
+  if (op->grid.dim == 2 && (!ws->r_alt || !ws->q_alt)) {
+    set_error("incomplete PCG workspace: 2D needs r_alt and q_alt");
+    return LSG_ERR_ARG;
+  }
+  if (op->grid.dim == 3 && !ws->p_ring) {
+    set_error("incomplete PCG workspace: 3D needs p_ring");
+    return LSG_ERR_ARG;
+  }
   return LSG_OK;
 }
+
+int64_t lsg_sizeof_op(void) { return (int64_t)sizeof(lsg_op); }
+int64_t lsg_sizeof_pcg_ws(void) { return (int64_t)sizeof(lsg_pcg_ws); }
+int64_t lsg_sizeof_grid(void) { return (int64_t)sizeof(lsg_grid); }
 
 int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol, double maxiter,
                   void *stream) {
   int rc = check_op(op);
-  if (!rc) rc = check_ws(ws);
+  if (!rc) rc = check_ws(op, ws);
   if (rc) return rc;
   return DISPATCH(op->grid, pcg_start(*op, *ws, rtol, atol, maxiter, S(stream)),
                   pcg_start(*op, *ws, rtol, atol, maxiter, S(stream)));
@@ -222,7 +238,7 @@ int lsg_pcg_start(const lsg_op *op, lsg_pcg_ws *ws, double rtol, double atol, do
 
 int lsg_pcg_iterate(const lsg_op *op, lsg_pcg_ws *ws, int32_t niter, void *stream) {
   int rc = check_op(op);
-  if (!rc) rc = check_ws(ws);
+  if (!rc) rc = check_ws(op, ws);
   if (rc) return rc;
   if (niter < 0) { set_error("niter must be >= 0"); return LSG_ERR_ARG; }
   return pcg_iterate_graph(*op, *ws, niter, S(stream));
@@ -234,7 +250,7 @@ void lsg_graph_stats(double *out4) {
 
 int lsg_pcg_finish(const lsg_op *op, lsg_pcg_ws *ws, void *stream) {
   int rc = check_op(op);
-  if (!rc) rc = check_ws(ws);
+  if (!rc) rc = check_ws(op, ws);
   if (rc) return rc;
   return DISPATCH(op->grid, pcg_finish(*op, *ws, S(stream)), pcg_finish(*op, *ws, S(stream)));
 }

@@ -20,6 +20,10 @@ int check_launch(const char *what);
 
 constexpr int kWarp = 32;
 
+// SM count of the current device (queried once per device): grids are sized in
+// multiples of it, and a cooperative grid may not exceed it times the CTAs per SM.
+int num_sms();
+
 // Programmatic dependent launch (PDL) for the PCG-iteration kernels: a kernel
 // launched with launch_pdl may have its CTAs scheduled while its predecessor
 // on the stream is still draining (hiding the launch and CTA-rasterisation

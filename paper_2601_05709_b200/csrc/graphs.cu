@@ -14,6 +14,7 @@
 // grid, k, parity, niter) does not: a miss on the exact key first re-captures
 // (host recording only) and updates an executable graph of the same shape in
 // place (cudaGraphExecUpdate), which is much cheaper than instantiating again.
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -49,7 +50,8 @@ struct Entry {
 std::mutex g_mu;
 std::vector<Entry> g_cache;
 unsigned long long g_clock = 0;
-cudaStream_t g_capture = nullptr;
+constexpr int kMaxDev = 64;
+cudaStream_t g_capture[kMaxDev] = {};  // one private capture stream per device
 constexpr size_t kMaxGraphs = 32;
 double g_stats[4] = {0, 0, 0, 0};  // hits, in-place updates, instantiations, host seconds
 
@@ -66,6 +68,19 @@ bool graphs_off() {
 }
 
 }  // namespace
+
+int num_sms() {
+  constexpr int kMaxDev = 64;
+  static int cache[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 148;
+  if (cache[dev] <= 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
 
 // 3D rotates three direction buffers (phase = iteration index mod 3), 2D two
 void advance_parity(const lsg_op &op, lsg_pcg_ws &ws, int niter) {
@@ -105,15 +120,18 @@ int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t 
     }
   }
   const auto t0 = std::chrono::steady_clock::now();
-  if (!g_capture && cudaStreamCreateWithFlags(&g_capture, cudaStreamNonBlocking) != cudaSuccess)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return check_launch("device");
+  cudaStream_t &cap = g_capture[dev];
+  if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess)
     return check_launch("capture stream");
   lsg_pcg_ws tmp = ws;
-  if (cudaStreamBeginCapture(g_capture, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+  if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return check_launch("begin capture");
-  int rc = (op.grid.dim == 2) ? d2::pcg_iterate(op, tmp, niter, g_capture)
-                              : d3::pcg_iterate(op, tmp, niter, g_capture);
+  int rc = (op.grid.dim == 2) ? d2::pcg_iterate(op, tmp, niter, cap)
+                              : d3::pcg_iterate(op, tmp, niter, cap);
   cudaGraph_t graph = nullptr;
-  cudaError_t ec = cudaStreamEndCapture(g_capture, &graph);
+  cudaError_t ec = cudaStreamEndCapture(cap, &graph);
   if (rc != LSG_OK) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
@@ -136,6 +154,10 @@ int pcg_iterate_graph(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t 
       return check_launch("graph launch");
     }
     cudaGetLastError();  // clear the failed update; instantiate instead
+    static const bool dbg = getenv("LSG_GRAPH_DEBUG") != nullptr;
+    if (dbg)
+      fprintf(stderr, "lsg graph: in-place update refused (result %d, dim %d, k %d, parity %d, niter %d)\n",
+              (int)info.result, op.grid.dim, ws.k, ws.parity, niter);
   }
   cudaGraphExec_t exec = nullptr;
   ec = cudaGraphInstantiate(&exec, graph, 0);

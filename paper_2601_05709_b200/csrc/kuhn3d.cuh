@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kEThreads, KE_MINB) kuhn_edge(ElastC ph, Geo g
   constexpr int NPA = NP > 0 ? NP : 1;
   constexpr int kSlotD = kERows * kEUSlot;  // doubles per ring slot
   constexpr int kSlotW = kERows * kEWSlot;  // words per ring slot
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   ESmem &S = *reinterpret_cast<ESmem *>(smem_raw);
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

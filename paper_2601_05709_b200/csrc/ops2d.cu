@@ -220,13 +220,12 @@ static int nstrips_of(const Geo &g) { return (int)ceil_div(g.nx + 1, kStrip); }
 // resident CTA slots of the 148 SMs (occupancy queried per kernel), which
 // keeps the one-halo-row-per-segment overhead small on large grids and avoids
 // a tail wave on small ones.
-constexpr int kSMs = 148;
 constexpr int kMaxPartials = 4096;  // >= CTAs per rhs of any launch below
 
 static int seg_for(const Geo &g, int k, int ctas_per_sm, int nstrips = -1) {
   const int64_t cols = ceil_div(nstrips < 0 ? nstrips_of(g) : nstrips, kWarps);
   const int64_t rows = g.ny + 1;
-  int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 4);
+  int64_t slots = (int64_t)num_sms() * (ctas_per_sm > 0 ? ctas_per_sm : 4);
   int64_t nseg = slots / (cols * k);
   if (nseg < 1) nseg = 1;
   int64_t seg = ceil_div(rows, nseg);
@@ -807,7 +806,7 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
     // tasks the longer march costs more than the barriers it saves (320x160: 7.9 vs 9.1)
     if (a.seg < 8) {
       const dim3 m8 = march_grid(g, 8, ws.k);
-      if ((int64_t)m8.x * m8.y * ws.k >= kSMs) a.seg = 8;
+      if ((int64_t)m8.x * m8.y * ws.k >= num_sms()) a.seg = 8;
     }
   }
   a.nstrips = nstrips_of(g);
@@ -821,17 +820,21 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
     const char *e = getenv("LSG_PERSIST_FILL");
     fill = e ? atoi(e) : 0;
   }
-  int ncta = (fill && ntask < kSMs) ? kSMs : ntask;
-  if (ncta > per_sm * kSMs) ncta = per_sm * kSMs;
+  int ncta = (fill && ntask < num_sms()) ? num_sms() : ntask;
+  if (ncta > per_sm * num_sms()) ncta = per_sm * num_sms();
   int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
   double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
   double *pbuf = ws.partials;
   PH phc = ph;
   Geo gc = g;
   void *args[] = {&phc, &gc, &a, &k, &tx, &ty, &niter, &parity, &re, &ro, &pe, &po, &qe, &qo, &pbuf};
-  if (cudaLaunchCooperativeKernel((void *)pcg_persistent<PH, KMAX>, dim3((unsigned)ncta),
-                                  dim3(kThreads), args, 0, st) != cudaSuccess)
-    return check_launch("pcg_persistent");
+  const cudaError_t le = cudaLaunchCooperativeKernel((void *)pcg_persistent<PH, KMAX>, dim3((unsigned)ncta),
+                                                     dim3(kThreads), args, 0, st);
+  if (le == cudaErrorCooperativeLaunchTooLarge) {  // e.g. a partitioned device: caller falls back
+    cudaGetLastError();
+    return 1;
+  }
+  if (le != cudaSuccess) return check_launch("pcg_persistent");
   ws.parity ^= (niter & 1);
   return check_launch("pcg_persistent");
 }

@@ -38,7 +38,6 @@ constexpr int kStrip = 30;
 #endif
 constexpr int kWarps = LSG_M3_WARPS;  // node rows per CTA (one of them halo)
 constexpr int kThreads = kWarps * 32;
-constexpr int kSMs = 148;
 constexpr int kMaxPartials = 4096;
 constexpr int kEwThreads = 256;
 constexpr double kA = 0.5854101966249685, kB = 0.1381966011250105;  // 4-point rule
@@ -937,7 +936,7 @@ static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int 
   // 32 planes (measured on cfg5: 16-32 planes, 3-4 waves are best; shorter
   // segments pay more halo planes, one wave leaves a tail).
   const int64_t per_seg = nstrips * tiles * k;
-  const int64_t slots = (int64_t)kSMs * (ctas_per_sm > 0 ? ctas_per_sm : 2);
+  const int64_t slots = (int64_t)num_sms() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
   static int waves = -1;  // LSG_M3_WAVES: target waves of CTAs (experiments)
   if (waves < 0) {
     const char *e = getenv("LSG_M3_WAVES");
@@ -1171,7 +1170,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   }
   auto grid_for = [&](int k) {
     int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
-    int64_t slots = (int64_t)kSMs * ew / k;
+    int64_t slots = (int64_t)num_sms() * ew / k;
     if (slots < 1) slots = 1;
     return dim3((unsigned)(need < slots ? need : slots), (unsigned)k);
   };
@@ -1248,7 +1247,7 @@ __global__ void clear_pending(int k, lsg_pcg_scalars *scal) {
 int pcg_finish(const lsg_op &op, lsg_pcg_ws &ws, cudaStream_t st) {
   const int64_t n = 3 * nodes_of(geo_of(op.grid));
   int64_t nb = ceil_div(n, kEwThreads);
-  if (nb > 4 * kSMs) nb = 4 * kSMs;
+  if (nb > 4 * num_sms()) nb = 4 * num_sms();
   pcg_finish_kernel<<<dim3((unsigned)nb, (unsigned)ws.k), kEwThreads, 0, st>>>(
       n, ws.p, ws.p_alt, ws.p_ring, ws.x, ws.scal);
   int rc = check_launch("pcg_finish3d");

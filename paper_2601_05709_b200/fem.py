@@ -302,15 +302,15 @@ class _Workspace:
             setattr(self.ws, name, getattr(self, name).data_ptr())
 
 
-_WS_CACHE = {}
-
-
 def _workspace(op, k):
-    key = (id(op.space.mesh), op.space.dof_count, k)
-    ws = _WS_CACHE.get(key)
+    """The PCG workspace of k right-hand sides on op's mesh.  Cached on the mesh object
+    (freed with it; never shared between meshes, dimensions or system sizes)."""
+    mesh = op.space.mesh
+    key = ("pcg_ws", mesh.dim, mesh.n, op.space.dof_count, k)
+    ws = mesh.device_cache.get(key)
     if ws is None:
         ws = _Workspace(op.grid, op.space.dof_count, k)
-        _WS_CACHE[key] = ws
+        mesh.device_cache[key] = ws
     return ws
 
 
@@ -326,7 +326,7 @@ def _scal(ws, field):
 # (a chunk is enqueued as power-of-two launches without polling in between).
 # Chunking never changes the iterates (the device decides convergence per
 # iteration); it only sets how often the host polls.
-_LAST_ITERS = {}
+_LAST_ITERS = {}  # (kind, dim, grid shape, n, k, rtol) -> iterations of the last solve
 _CHUNK_DOUBLING = os.environ.get("LSG_CHUNK_DOUBLING") == "1"  # A/B: the plain doubling plan
 
 
@@ -394,7 +394,7 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
     ev.synchronize()
     done = _scal(ws, "done")
     prof = PCG_PROFILE
-    key = (op.kind, id(op.space.mesh), n, k, float(rtol))
+    key = (op.kind, op.space.mesh.dim, op.space.mesh.n, n, k, float(rtol))
     if chunk is not None:
         plan = itertools.repeat(int(chunk))
     else:

@@ -100,15 +100,14 @@ def initial_level(spec, space):
 
 
 class _Scratch:
-    def __init__(self):
-        self.cache = {}
+    """Per-mesh device scratch buffers, cached on the mesh object (freed with it)."""
 
     def get(self, mesh, name, numel, dtype=torch.float64):
-        key = (id(mesh), name, numel, dtype)
-        t = self.cache.get(key)
+        key = ("scratch", name, numel, dtype)
+        t = mesh.device_cache.get(key)
         if t is None:
             t = torch.empty(numel, dtype=dtype, device="cuda")
-            self.cache[key] = t
+            mesh.device_cache[key] = t
         return t
 
 

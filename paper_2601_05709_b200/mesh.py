@@ -40,6 +40,9 @@ class StructuredMesh:
         if facet_tags is None:
             facet_tags = np.zeros(len(self.boundary_facets), dtype=np.int32)
         self.facet_tags = np.asarray(facet_tags, dtype=np.int32)
+        # device workspaces / scratch buffers of solves on this mesh (fem._workspace,
+        # levelset._Scratch): they live and die with the mesh object
+        self.device_cache = {}
 
     # -- sizes --------------------------------------------------------------------
     @property

@@ -1,8 +1,13 @@
 import os
 import sys
 
-import numpy as np
-import pytest
+# one BLAS thread per process: the oracle's scipy cg is a chain of small BLAS
+# calls, which threaded OpenBLAS slows down ~50x on a shared host
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

@@ -18,10 +18,16 @@ the reference's own run() history in 2D (tests/test_oracle.py); the 3D pieces
 are restatements (property-pinned).
 """
 
-import multiprocessing as mp
 import os
-import sys
-import time
+
+# one BLAS thread per process: the oracle's scipy cg is a chain of small BLAS
+# calls, and threaded OpenBLAS on a shared host makes each ~50x slower
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import multiprocessing as mp  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
 
 import numpy as np
 
