@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
   double *xchg = stage + Stage<PH, ACT>::doubles;                      // [2][kWarps][2*NOUT][32]
   uint32_t *stw = reinterpret_cast<uint32_t *>(xchg + Stage<PH, ACT>::xchg);  // [3][kWarps+1][32]
   __shared__ double scratch[NPA * kWarps];
-  __shared__ double wtab[16];  // per-tet weights (physics with kTable)
+  __shared__ double wtab[24];  // per-tet weights (physics with kTable)
   if constexpr (ACT == PCGQ) pdl_wait();  // launched with launch_pdl (see common.cuh)
   if constexpr (PH::kTable) ph.fill_table(wtab, threadIdx.x);
   auto SR = [&](int slot, int row, int s) -> double * {

@@ -293,8 +293,6 @@ static int launch_march(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march<PH, ACT, uint8_t>,
                                                       kThreads, 0) != cudaSuccess)
       ctas_per_sm = 4;
-    const char *e = getenv("LSG_M2_GRID_CTAS");  // experiment: size the grid for this many
-    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
   }
   a.seg = seg_for(g, k, ctas_per_sm);
   a.nstrips = nstrips_of(g);
@@ -322,8 +320,6 @@ static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH, A>,
                                                       kThreads, 0) != cudaSuccess)
       ctas_per_sm = 4;
-    const char *e = getenv("LSG_M2_GRID_CTAS");
-    if (e && atoi(e) > 0) ctas_per_sm = atoi(e);
   }
   a.nstrips = (int)ceil_div(g.nx + 1, kStripRq);
   a.seg = seg_for(g, k, ctas_per_sm, a.nstrips);
@@ -792,15 +788,8 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
     ctas_march = 4;
   a.seg = seg_for(g, ws.k, ctas_march);
   {
-    // LSG_PERSIST_SEGMIN: minimum rows per task (experiments; cfg1: 4 rows 7.0 us,
-    // 8 rows 8.6, 16 rows 11.7 -- the per-iteration barrier and reductions are
-    // cheaper than the longer march)
-    static int segmin = -1;
-    if (segmin < 0) {
-      const char *e = getenv("LSG_PERSIST_SEGMIN");
-      segmin = e ? atoi(e) : 0;
-    }
-    if (a.seg < segmin) a.seg = segmin;
+    // (short tasks win on small grids -- cfg1: 4 rows 7.0 us, 8 rows 8.6, 16 rows
+    // 11.7: the per-iteration barrier and reductions are cheaper than a longer march)
     // mid-size systems: 8-row tasks while that still gives every SM one (velocity
     // solve of cfg2, 1024x256: 14.5 -> 13.2 us; 512x256: 12.3 -> 10.8 us); with fewer
     // tasks the longer march costs more than the barriers it saves (320x160: 7.9 vs 9.1)
@@ -813,14 +802,8 @@ static int launch_persistent_k(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &
   const dim3 mg = march_grid(g, a.seg, ws.k);
   const int ntask = (int)(mg.x * mg.y * ws.k);
   // one task per CTA (cfg1 PCG iteration 7.9 -> 7.0 us against filling every SM:
-  // fewer partials to reduce and CTAs to barrier); LSG_PERSIST_FILL=1: at
-  // least one CTA per SM
-  static int fill = -1;
-  if (fill < 0) {
-    const char *e = getenv("LSG_PERSIST_FILL");
-    fill = e ? atoi(e) : 0;
-  }
-  int ncta = (fill && ntask < num_sms()) ? num_sms() : ntask;
+  // fewer partials to reduce and CTAs to barrier)
+  int ncta = ntask;
   if (ncta > per_sm * num_sms()) ncta = per_sm * num_sms();
   int k = ws.k, tx = (int)mg.x, ty = (int)mg.y, parity = ws.parity;
   double *re = ws.r, *ro = ws.r_alt, *pe = ws.p, *po = ws.p_alt, *qe = ws.q, *qo = ws.q_alt;
@@ -851,11 +834,7 @@ static int launch_persistent(const PH &ph, const Geo &g, MArgs a, lsg_pcg_ws &ws
 // on large ones the work does and the grid barriers + cross-CTA reductions
 // would cost more than the launches they replace (cfg2: 112 vs 59 us).
 bool pcg_persistent_ok(const lsg_op &op, const lsg_pcg_ws &ws) {
-  static int64_t limit = -1;  // LSG_PCG2D_PERSIST_MAX: dofs x rhs threshold
-  if (limit < 0) {
-    const char *e = getenv("LSG_PCG2D_PERSIST_MAX");
-    limit = e ? atoll(e) : 600000;
-  }
+  constexpr int64_t limit = 600000;  // dofs x rhs (cfg1 and the velocity solves: yes; cfg2 state: no)
   if (!persistent_on() || ws.k > 8 || op.grid.dim != 2) return false;
   if (op.kind != LSG_OP_ELASTICITY && op.kind != LSG_OP_H1 && op.kind != LSG_OP_LAPLACE) return false;
   const int64_t nn = (int64_t)(op.grid.n[0] + 1) * (op.grid.n[1] + 1);

@@ -118,77 +118,86 @@ struct Elast {
   }
 };
 
-// Cubic cells (h_x = h_y = h_z, cfg3 and cfg5): the fluxes are the columns of
-// the symmetric stress scaled by one 1/h, so with s = w mu/h^2, l = w lam/h^2
-//   T_d[q] = s (D_d[q] + D_q[d])  (q != d, shared by T_d and T_q),
-//   T_d[d] = 2 s D_d[d] + l (D_0[0] + D_1[1] + D_2[2]),
-// the weight is folded into s and l, and each corner's first contribution is
-// a plain write (compile-time first-touch), about 20% fewer fp64 instructions
-// per cell than the general form above.
+// Cubic cells (h_x = h_y = h_z, cfg3 and cfg5): with s = w mu/h^2, l = w lam/h^2
+// (w = |T| times the tet's ersatz weight) and the raw edge differences D^x,
+// D^y, D^z along the tet's x-, y- and z-directed path edges, the stress is
+//   sigma_aa = l (D^x_x + D^y_y + D^z_z) + 2 s D^a_a,  sigma_ab = s (D^a_b + D^b_a),
+// and the tet adds the column sigma e_a to the flux of its a-directed edge (the
+// edge's start corner receives -flux, its end corner +flux).  Every path edge
+// is one of the cube's 12 edges, so the cell evaluates each edge difference
+// once (36 subtractions instead of 54), sums the fluxes of the tets sharing an
+// edge, and forms each corner's contribution as the divergence of its three
+// edges: ~170 fp64 instructions per cell and field against ~240 tet by tet.
 struct ElastC {
   static constexpr int NIN = 3, NOUT = 3;
   static constexpr bool kTable = true;  // per-CTA shared table of the tet weights
   double w0, w1;  // |T| (inside n + outside (4-n)) / 4 = w0 + w1 n
   double cs, cl;  // mu / h^2, lam / h^2
 
-  // tab[n] = w(n) mu/h^2, tab[8 + n] = w(n) lam/h^2 for n = 0..4; index 7
-  // (what invalid cells look up) gives 0
+  // tab[n] = w(n) mu/h^2, tab[8 + n] = w(n) lam/h^2, tab[16 + n] = 2 w(n) mu/h^2
+  // for n = 0..4; index 7 (what invalid cells look up) gives 0
   __device__ __forceinline__ void fill_table(double *tab, int t) const {
-    if (t < 16) {
+    if (t < 24) {
       const int n = t & 7;
       const double w = n <= 4 ? fma((double)n, w1, w0) : 0.0;
-      tab[t] = w * (t < 8 ? cs : cl);
+      tab[t] = t < 8 ? w * cs : t < 16 ? w * cl : 2.0 * (w * cs);
     }
   }
   __device__ __forceinline__ static bool valid(uint32_t w) { return Elast::valid(w); }
   __device__ __forceinline__ static uint32_t mask(uint32_t w) { return Elast::mask(w); }
 
-  // does a tet with index < M touch corner v?
-  static __host__ __device__ constexpr bool touched(int M, int v) {
-    return M > 0 && (v == 0 || v == 7 || corner(M - 1, 1) == v || corner(M - 1, 2) == v ||
-                     touched(M - 1, v));
-  }
-  template <int M, int V>
-  __device__ __forceinline__ static void put(double (*c)[NOUT], int q, double x) {
-    if constexpr (touched(M, V)) c[V][q] += x; else c[V][q] = x;
-  }
-
+  // the six stress components (xx, yy, zz, xy, xz, yz) of tet M
   template <int M>
-  __device__ __forceinline__ void tet(const double (*u)[NIN], uint32_t nbits, const double *tab,
-                                      double (*c)[NOUT]) const {
-    constexpr int a = perm(M, 0), b = perm(M, 1), cc = perm(M, 2);
-    constexpr int P0 = 0, P1 = corner(M, 1), P2 = corner(M, 2), P3 = 7;
+  __device__ __forceinline__ static void sigma(const double *Dx, const double *Dy, const double *Dz,
+                                               uint32_t nbits, const double *tab, double (&sg)[6]) {
     const uint32_t n = (nbits >> (3 * M)) & 7u;
-    const double s = tab[n], l = tab[8 + n];
-    double D[3][3];  // D[axis][comp]
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      D[a][q] = u[P1][q] - u[P0][q];
-      D[b][q] = u[P2][q] - u[P1][q];
-      D[cc][q] = u[P3][q] - u[P2][q];
-    }
-    const double lt = l * (D[0][0] + D[1][1] + D[2][2]);
-    const double s2 = s + s;
-    double T[3][3];
-    T[0][1] = T[1][0] = s * (D[0][1] + D[1][0]);
-    T[0][2] = T[2][0] = s * (D[0][2] + D[2][0]);
-    T[1][2] = T[2][1] = s * (D[1][2] + D[2][1]);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) T[d][d] = fma(s2, D[d][d], lt);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      put<M, P0>(c, q, -T[a][q]);
-      put<M, P1>(c, q, T[a][q] - T[b][q]);
-      put<M, P2>(c, q, T[b][q] - T[cc][q]);
-      put<M, P3>(c, q, T[cc][q]);
-    }
+    const double s = tab[n], l = tab[8 + n], s2 = tab[16 + n];
+    const double lt = l * (Dx[0] + Dy[1] + Dz[2]);
+    sg[0] = fma(s2, Dx[0], lt);
+    sg[1] = fma(s2, Dy[1], lt);
+    sg[2] = fma(s2, Dz[2], lt);
+    sg[3] = s * (Dx[1] + Dy[0]);
+    sg[4] = s * (Dx[2] + Dz[0]);
+    sg[5] = s * (Dy[2] + Dz[1]);
   }
 
   __device__ __forceinline__ void cell(const double (*u)[NIN], uint32_t word, int, int, int,
                                        double (*c)[NOUT], const double *tab) const {
     const uint32_t nb = valid(word) ? word : 0x3ffffu;  // invalid: every tet reads index 7
-    tet<0>(u, nb, tab, c); tet<1>(u, nb, tab, c); tet<2>(u, nb, tab, c);
-    tet<3>(u, nb, tab, c); tet<4>(u, nb, tab, c); tet<5>(u, nb, tab, c);
+    // cell edges (corner bits x = 1, y = 2, z = 4): X_yz from corner 2y+4z,
+    // Y_xz from x+4z, Z_xy from x+2y
+    double X00[3], X10[3], X01[3], X11[3], Y00[3], Y10[3], Y01[3], Y11[3], Z00[3], Z10[3], Z01[3], Z11[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      X00[q] = u[1][q] - u[0][q]; X10[q] = u[3][q] - u[2][q]; X01[q] = u[5][q] - u[4][q]; X11[q] = u[7][q] - u[6][q];
+      Y00[q] = u[2][q] - u[0][q]; Y10[q] = u[3][q] - u[1][q]; Y01[q] = u[6][q] - u[4][q]; Y11[q] = u[7][q] - u[5][q];
+      Z00[q] = u[4][q] - u[0][q]; Z10[q] = u[5][q] - u[1][q]; Z01[q] = u[6][q] - u[2][q]; Z11[q] = u[7][q] - u[3][q];
+    }
+    // tets (perm): 0 (x,y,z) X00 Y10 Z11, 1 (x,z,y) X00 Y11 Z10, 2 (y,x,z) X10 Y00 Z11,
+    //              3 (y,z,x) X11 Y00 Z01, 4 (z,x,y) X01 Y11 Z00, 5 (z,y,x) X11 Y01 Z00
+    double s0[6], s1[6], s2[6], s3[6], s4[6], s5[6];
+    sigma<0>(X00, Y10, Z11, nb, tab, s0);
+    sigma<1>(X00, Y11, Z10, nb, tab, s1);
+    sigma<2>(X10, Y00, Z11, nb, tab, s2);
+    sigma<3>(X11, Y00, Z01, nb, tab, s3);
+    sigma<4>(X01, Y11, Z00, nb, tab, s4);
+    sigma<5>(X11, Y01, Z00, nb, tab, s5);
+    // flux columns: x-edge (xx, xy, xz), y-edge (xy, yy, yz), z-edge (xz, yz, zz)
+    constexpr int CX[3] = {0, 3, 4}, CY[3] = {3, 1, 5}, CZ[3] = {4, 5, 2};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double fx00 = s0[CX[q]] + s1[CX[q]], fx10 = s2[CX[q]], fx01 = s4[CX[q]], fx11 = s3[CX[q]] + s5[CX[q]];
+      const double fy00 = s2[CY[q]] + s3[CY[q]], fy10 = s0[CY[q]], fy01 = s5[CY[q]], fy11 = s1[CY[q]] + s4[CY[q]];
+      const double fz00 = s4[CZ[q]] + s5[CZ[q]], fz10 = s1[CZ[q]], fz01 = s3[CZ[q]], fz11 = s0[CZ[q]] + s2[CZ[q]];
+      c[0][q] = -(fx00 + fy00) - fz00;
+      c[1][q] = (fx00 - fy10) - fz10;
+      c[2][q] = (fy00 - fx10) - fz01;
+      c[3][q] = (fx10 + fy10) - fz11;
+      c[4][q] = (fz00 - fx01) - fy01;
+      c[5][q] = (fx01 + fz10) - fy11;
+      c[6][q] = (fy01 + fz01) - fx11;
+      c[7][q] = (fx11 + fy11) + fz11;
+    }
   }
 };
 
@@ -937,27 +946,13 @@ static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int 
   // segments pay more halo planes, one wave leaves a tail).
   const int64_t per_seg = nstrips * tiles * k;
   const int64_t slots = (int64_t)num_sms() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  static int waves = -1;  // LSG_M3_WAVES: target waves of CTAs (experiments)
-  if (waves < 0) {
-    const char *e = getenv("LSG_M3_WAVES");
-    waves = e ? atoi(e) : 0;
-  }
-  const int64_t wv = waves > 0 ? waves : default_waves;
+  const int64_t wv = default_waves;
   int64_t ns = ceil_div(wv * slots, per_seg);
   if (ns < 1) ns = 1;
   int64_t s = ceil_div(g.nz + 1, ns);
-  static int smax = -1;  // LSG_M3_SEGMAX: cap on planes per segment (experiments)
-  if (smax < 0) {
-    const char *e = getenv("LSG_M3_SEGMAX");
-    smax = e ? atoi(e) : 32;
-    if (smax < 6) smax = 6;
-  }
-  static int smin = -1;  // LSG_M3_SEGMIN: floor on planes per segment (experiments)
-  if (smin < 0) {
-    const char *e = getenv("LSG_M3_SEGMIN");
-    smin = e ? atoi(e) : 5;  // cfg3: 5 planes fill one wave (PCG 28.2 -> 26.6 us, apply 20.6 -> 18.5)
-    if (smin < 2) smin = 2;
-  }
+  // measured: segments of 5..32 planes (cfg3: 5 planes fill one wave, PCG
+  // iteration 28.2 -> 26.6 us; cfg5: 16-32 planes, 3-4 waves)
+  constexpr int64_t smax = 32, smin = 5;
   if (s > smax) s = smax;
   if (s < smin) s = smin;
   while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
@@ -1162,12 +1157,7 @@ static int streams3d() {
 
 int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   const int64_t n = 3 * nodes_of(geo_of(op.grid));
-  static int ew = -1;  // LSG_EW_CTAS: elementwise CTAs per SM (experiments)
-  if (ew < 0) {
-    const char *e = getenv("LSG_EW_CTAS");
-    ew = e ? atoi(e) : 4;
-    if (ew < 1) ew = 1;
-  }
+  constexpr int ew = 4;  // elementwise CTAs per SM: the grid is one wave at 4 CTAs/SM
   auto grid_for = [&](int k) {
     int64_t need = ceil_div(n, (int64_t)kEwThreads * 4);
     int64_t slots = (int64_t)num_sms() * ew / k;

@@ -16,7 +16,6 @@
 """
 
 import itertools
-import os
 
 import numpy as np
 import torch
@@ -327,7 +326,6 @@ def _scal(ws, field):
 # Chunking never changes the iterates (the device decides convergence per
 # iteration); it only sets how often the host polls.
 _LAST_ITERS = {}  # (kind, dim, grid shape, n, k, rtol) -> iterations of the last solve
-_CHUNK_DOUBLING = os.environ.get("LSG_CHUNK_DOUBLING") == "1"  # A/B: the plain doubling plan
 
 
 def _pieces(total):
@@ -398,7 +396,7 @@ def solve_batched(op, rhs, x0=None, rtol=CG_RTOL, atol=CG_ATOL, maxiter=None, ch
     if chunk is not None:
         plan = itertools.repeat(int(chunk))
     else:
-        plan = _chunks(None if _CHUNK_DOUBLING else _LAST_ITERS.get(key))
+        plan = _chunks(_LAST_ITERS.get(key))
     while not bool((done != 0).all()):
         chunk = next(plan)
         if prof is not None:
