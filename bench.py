@@ -336,7 +336,7 @@ def largest_applies(hbm, ncu):
         u = torch.randn((k, dim * N), dtype=torch.float64, device="cuda")
         ms = flushed_apply_ms(op, u)
         byts = 16.0 * dim * k * N + E
-        kern = ncu.get(f"apply_{name}", {})
+        kern = {k: v for k, v in ncu.get(f"apply_{name}", {}).items() if k != "launches"}
         out[name] = {"grid": "x".join(map(str, n)), "k": k, "ms": ms, "dof_per_s": k * dim * N / (ms / 1e3),
                      "gbs": byts / (ms / 1e3) / 1e9, "frac": byts / (ms / 1e3) / 1e9 / hbm, "bytes": byts,
                      "ncu": kern or None}
@@ -404,8 +404,7 @@ def pcg_roofline(lw, hbm, peak_kind, ncu):
     pcg_bytes = 80.0 * d * N * rhs_iters + (16.0 * d * N + E) * max_iters
     achieved = pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms > 0 else 0.0
     all_ms = sum(p["events"][0].elapsed_time(p["events"][1]) for p in prof)
-    key = f"pcg{d}d"
-    kern = ncu.get(key, {})
+    kern = ncu.get(f"pcg{d}d", {})
     traffic = kern.get("dram_bytes_per_iteration")
     return {"bound": "hbm", "kernel": PCG_KERNELS[d], "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,

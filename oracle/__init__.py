@@ -2,7 +2,12 @@
 
 This package is a numpy/scipy restatement of the reference algorithm
 (``/root/reference/pkg/src/lsopt``, ``lsopt`` 0.1.0) for the north-star hot
-path, written from the reference's formulas, never copied.  It exists to
+path.  Most of it is written from the reference's formulas; the one exception
+is the reference's own Crank-Nicolson Petrov-Galerkin transport / PG-AB2
+reinitialisation (``levelset.transport_pg`` / ``reinitialize_pg`` and their
+helpers, ``levelset.py:177-287`` here), which follows the reference's code
+(``levelset.py:109-278``) closely on purpose: it has to reproduce that
+scheme's floating-point behaviour to pin the device PG scheme.  It exists to
 check the CUDA path, never to stand in for it: only ``tests/``,
 ``__graft_entry__.smoke()`` and the ``cpu_baseline`` / ``--impl reference``
 legs of ``bench.py`` may import it.  The product package
@@ -30,9 +35,11 @@ Modules
 grid       structured rectangle / box meshes (mesh.py:113-198 restated, + Kuhn tets)
 fem        P1 spaces, element kernels, CSR assembly, Dirichlet elimination,
            Jacobi-PCG via scipy ``cg`` (fem.py:56-466 restated, d = 2, 3)
-levelset   explicit upwind transport + Godunov reinitialisation (restated spec)
-velocity   H1 velocity form and solve (velocity.py:32-159 restated)
-ppl        proximal-perturbed Lagrangian recursion (ppl.py:47-114 restated)
-model      compliance model (models/compliance.py:37-156, base.py:100-158)
+levelset   explicit upwind transport + Godunov reinitialisation (restated spec),
+           and the reference's CN/PG scheme (levelset.py:109-278)
+model      compliance / heat / inverse models (models/*.py restated), the H1
+           velocity form and solve (velocity.py:32-159; SuperLU, or Jacobi-CG to
+           1e-14 for large 3D fixtures), PPL recursion (ppl.py:47-114)
 driver     outer loop (driver.py:121-298 restated)
+cases      the BASELINE configurations assembled for the oracle
 """

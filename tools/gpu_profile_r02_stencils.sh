@@ -14,11 +14,3 @@ cap() {  # name, kernel regex, count, command...
 KEEP=keep cap r02_apply_cfg5 'march3s<lsg::d3::ElastC, .int.0>' 1 python tools/prof_apply3d.py --grid 192x96x96 --k 4 --applies 1
 KEEP= cap r02_pcg_cfg5 'ElastC, .int.5|pcg_prep|pcg_update' 6 python tools/prof_apply3d.py --grid 192x96x96 --k 4 --pcg 3 --applies 1
 KEEP= cap r02_apply_cfg4 'march<lsg::d2::Elast, .int.0' 1 python tools/prof_apply3d.py --grid 4096x2048 --k 1 --applies 1
-KEEP= cap r02_pcg_cfg4 'march_pcg_rqs' 1 python tools/prof_apply3d.py --grid 4096x2048 --k 1 --pcg 3 --applies 1
-KEEP= cap r02_pcg_cfg2 'march_pcg_rqs' 1 python tools/prof_apply3d.py --grid 1024x256 --k 8 --pcg 3 --applies 1
-KEEP= cap r02_loop_cfg5 'Shape|H1P, 5|transport|reinit' 8 python tools/prof_loop.py --config cfg5
-KEEP= cap r02_loop_cfg2 'Shape|march_pcg_rqs_kernel<lsg::d2::H1|transport|reinit' 8 python tools/prof_loop.py --config cfg2
-ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -c 800 --csv \
-  --log-file $O/r02_launches_cfg5.csv python bench.py --warmup 1 --steps 1 --no-cpu-baseline --no-e2e \
-  --no-secondary --no-largest > $O/launches.log 2>&1; echo "launches rc=$?"
-du -sh $O
