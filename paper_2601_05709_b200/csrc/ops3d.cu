@@ -506,7 +506,6 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 }  // namespace lsg
 
 #include "march3s.cuh"
-#include "kuhn3d.cuh"
 
 namespace lsg {
 namespace d3 {
@@ -938,9 +937,9 @@ static H1P make_h1_plain(const Geo &g, const lsg_op &op) {
 int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 
 static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid,
-                            int default_waves = 3, int strip = kStrip, int rows = kWarps - 1) {
-  const int64_t nstrips = ceil_div(g.nx + 1, strip);
-  const int64_t tiles = ceil_div(g.ny + 1, rows);
+                            int default_waves = 3) {
+  const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
+  const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
   // z-segments (one halo plane each) sized for ~3 waves of CTAs and at most
   // 32 planes (measured on cfg5: 16-32 planes, 3-4 waves are best; shorter
   // segments pay more halo planes, one wave leaves a tail).
@@ -985,51 +984,12 @@ static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   return check_launch("march3d");
 }
 
-// The lattice-edge elasticity kernel (kuhn3d.cuh) for cubic cells: fewer
-// fp64 instructions, but register- and issue-bound at 2 CTAs/SM (measured
-// slower than march3s<ElastC>: cfg5 apply 338 vs 233 us); opt-in for A/B
-// with LSG_KUHN_EDGE=1.
-static bool use_edge_kernel() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("LSG_KUHN_EDGE");
-    v = e ? atoi(e) : 0;
-  }
-  return v != 0;
-}
-
-template <int ACT>
-static int launch_edge(const ElastC &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
-  static int ctas = -1;
-  constexpr size_t smem = sizeof(ESmem);
-  if (ctas < 0) {
-    cudaFuncSetAttribute(kuhn_edge<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kuhn_edge<ACT>, kEThreads, smem) != cudaSuccess)
-      ctas = 2;
-  }
-  dim3 grid;
-  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid, ACT == PCGQ ? 2 : 3, kEStrip, kEWarps - 1);
-  a.nstrips = (int)ceil_div(g.nx + 1, kEStrip);
-  if (ACT == PCGQ) {
-    if (launch_pdl(kuhn_edge<ACT>, grid, dim3(kEThreads), smem, st, ph, g, a) != cudaSuccess)
-      return check_launch("kuhn_edge launch");
-  } else {
-    kuhn_edge<ACT><<<grid, kEThreads, smem, st>>>(ph, g, a);
-  }
-  return check_launch("kuhn_edge");
-}
-
 template <int ACT>
 static int dispatch(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   a.words = static_cast<const uint32_t *>(op.words);
   if (op.kind == LSG_OP_ELASTICITY) {
-    if (is_cubic(g)) {
-      if constexpr (ACT == APPLY || ACT == RESID || ACT == PCGQ) {
-        if (use_edge_kernel()) return launch_edge<ACT>(make_elast_cubic(g, op), g, a, k, st);
-      }
-      return launch<ElastC, ACT>(make_elast_cubic(g, op), g, a, k, st);
-    }
+    if (is_cubic(g)) return launch<ElastC, ACT>(make_elast_cubic(g, op), g, a, k, st);
     return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
   }
   if (op.kind == LSG_OP_H1) {

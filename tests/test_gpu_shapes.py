@@ -3,9 +3,7 @@
 The stencil kernels tile the lattice (2D: 30 owned columns per warp, 4 warps
 per CTA, row segments marched per CTA; 3D: 30 columns x 7 owned rows per CTA,
 z segments, cp.async staging of 16-byte row chunks with a separate path for
-the array's last row; 3D cubic elasticity: 31 columns x 7 owned rows per CTA,
-bulk-copy staging with a plain-load path for windows at either end of the
-array).  These shapes sit on and around every tile edge,
+the array's last row).  These shapes sit on and around every tile edge,
 include single-cell axes, and use a seeded random level set so every material
 count 0..nq occurs.  Gates as the north star: apply / diagonal / S1 vector /
 one level-set step <= 1e-10 (diagonal 1e-12), CG solutions <= 1e-8.
