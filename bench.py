@@ -207,7 +207,7 @@ def cpu_units(c, procs, slab=None, cg_iters=6, vel_iters=6):
     n = tuple(c.n)
     full_cells = float(np.prod(n))
     if slab is None:
-        slab = max(1, int(round(n[-1] / 32))) if c.dim == 3 else max(2, int(round(n[-1] / 16)))
+        slab = max(1, int(round(n[-1] / 48))) if c.dim == 3 else max(2, int(round(n[-1] / 16)))
     slab = min(slab, n[-1])
     h_last = (c.hi[-1] - c.lo[-1]) / n[-1]
     # slab of the mesh; clamp on x = lo and the k load cases on the x = hi face, so that
