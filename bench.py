@@ -317,8 +317,8 @@ def largest_applies(hbm, ncu):
     Bytes: 16 d k N + E (material 1 B per element)."""
     import torch
 
-    from paper_2601_05709_b200 import build_box_mesh, build_rect_mesh
-    from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace
+    from paper_2601_05709_b200 import _lib, build_box_mesh, build_rect_mesh
+    from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace, _workspace
 
     out = {}
     for name, dim, n, k in (("cfg4", 2, (4096, 2048), 1), ("cfg5", 3, (192, 96, 96), 4)):
@@ -336,11 +336,32 @@ def largest_applies(hbm, ncu):
         u = torch.randn((k, dim * N), dtype=torch.float64, device="cuda")
         ms = flushed_apply_ms(op, u)
         byts = 16.0 * dim * k * N + E
-        kern = {k: v for k, v in ncu.get(f"apply_{name}", {}).items() if k != "launches"}
+        kern = {key: v for key, v in ncu.get(f"apply_{name}", {}).items() if key != "launches"}
         out[name] = {"grid": "x".join(map(str, n)), "k": k, "ms": ms, "dof_per_s": k * dim * N / (ms / 1e3),
                      "gbs": byts / (ms / 1e3) / 1e9, "frac": byts / (ms / 1e3) / 1e9 / hbm, "bytes": byts,
                      "ncu": kern or None}
-        del op, u
+        # the fused PCG iteration standalone (stopping disabled: rtol = atol = 0), the north
+        # star's "fused CG >= 60% of HBM on the largest meshes"; (80k+16) d N + E bytes
+        ws = _workspace(op, k)
+        ws.b.copy_(torch.randn((k, dim * N), dtype=torch.float64, device="cuda"))
+        ws.x.zero_()
+        ws.ws.dinv = op.inverse_diagonal().data_ptr()
+        cop, st = op._op(), _lib.stream()
+        _lib.call("lsg_pcg_start", cop, ws.ws, 0.0, 0.0, 1e12, st)
+        _lib.call("lsg_pcg_iterate", cop, ws.ws, 32, st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        _lib.call("lsg_pcg_iterate", cop, ws.ws, 64, st)
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 64
+        pbytes = (80.0 * k + 16.0) * dim * N + E
+        out[name]["pcg"] = {"us_per_iteration": us, "gbs": pbytes / (us * 1e-6) / 1e9,
+                            "frac": pbytes / (us * 1e-6) / 1e9 / hbm, "bytes": pbytes,
+                            "note": "standalone fused PCG iteration (64 iterations after 32, stopping "
+                                    "disabled), canonical two-pass bytes"}
+        del op, u, ws
     return out
 
 
