@@ -425,8 +425,13 @@ def pcg_roofline(lw, hbm, peak_kind, ncu):
     pcg_bytes = 80.0 * d * N * rhs_iters + (16.0 * d * N + E) * max_iters
     achieved = pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms > 0 else 0.0
     all_ms = sum(p["events"][0].elapsed_time(p["events"][1]) for p in prof)
-    kern = ncu.get(f"pcg{d}d", {})
+    kern = dict(ncu.get(f"pcg{d}d", {}))
     traffic = kern.get("dram_bytes_per_iteration")
+    launches = ncu.get("pcg_cfg5" if d == 3 else "pcg_cfg2", {}).get("launches", [])
+    if launches:  # per-launch split of one batched iteration (ncu, cold, serialised)
+        kern["split_us"] = [[r["kernel"].split("(")[0].replace("void ", ""), round(r.get("us", 0.0), 1),
+                             round((r.get("dram_read", 0.0) + r.get("dram_write", 0.0)) / 1e6, 1)]
+                            for r in launches]
     return {"bound": "hbm", "kernel": PCG_KERNELS[d], "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
             "bytes_per_iteration": "(80k+16) d N + E per k-rhs iteration (canonical two-pass)",
