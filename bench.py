@@ -636,7 +636,7 @@ def reference_arm(args, world, rank, local):
                           "note": "value = 1 / s_per_outer_iteration; each step measured the per-unit "
                                   "costs on a slab and extrapolated; ms_per_step is the step's real "
                                   "duration"},
-        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": units["pcg_procs"], "kind": "port",
                          "sample": f"per step: oracle (numpy/scipy restatement of the reference) on a "
                                    f"{units['slab']} slab of {args.config}, scaled x{units['scale']:.0f}: "
                                    f"assembly + elimination, scipy-cg PCG iterations ({units['pcg_procs']} "
