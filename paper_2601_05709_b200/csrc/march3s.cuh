@@ -36,18 +36,6 @@ struct Stage {
 #ifndef LSG_M3_MINB
 #define LSG_M3_MINB 2
 #endif
-#ifndef LSG_M3_PAIRBAR
-#define LSG_M3_PAIRBAR 0
-#endif
-
-// Per-plane synchronisation of warp row w with its two neighbours only (named
-// barriers 1..kWarps-1 of 64 threads each: barrier b joins warps b-1 and b).
-// A warp depends on the staged rows and the y-contributions of the adjacent
-// warps, not on the whole CTA.
-__device__ __forceinline__ void pair_sync(int w) {
-  if (w > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(w) : "memory");
-  if (w < kWarps - 1) asm volatile("bar.sync %0, 64;\n" ::"r"(w + 1) : "memory");
-}
 
 template <class PH, int ACT>
 __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, MArgs a) {
@@ -279,11 +267,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
     if constexpr (ACT == SHAPE) {
       ph.cell(U, c.wc, own && (kk - 1) >= K0, C, part);
     } else {
-#ifdef LSG_M3S_PROG
-      if constexpr (PH::kTable) ph.cell_prog(U, c.wc, C, wtab);
-#else
       if constexpr (PH::kTable) ph.cell(U, c.wc, i, jw, kk - 1, C, wtab);
-#endif
       else ph.cell(U, c.wc, i, jw, kk - 1, C);
     }
     double T[4][NOUT];
@@ -298,8 +282,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
       SC(par, w, NOUT + t, lane) = T[3][t];
     }
     cp_async_wait<1>();  // plane kk+1 has landed (kk+2 may still be in flight)
-    if constexpr (LSG_M3_PAIRBAR) pair_sync(w);
-    else __syncthreads();
+    __syncthreads();
 #pragma unroll
     for (int t = 0; t < NOUT; ++t) {
       acc_c[t] += T[0][t] + SC(par, wm1, t, lane);

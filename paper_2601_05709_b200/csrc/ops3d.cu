@@ -146,29 +146,6 @@ struct ElastC {
   __device__ __forceinline__ static bool valid(uint32_t w) { return Elast::valid(w); }
   __device__ __forceinline__ static uint32_t mask(uint32_t w) { return Elast::mask(w); }
 
-  // paired table for 16-byte lookups: tab2[n] = (w(n) mu/h^2, w(n) lam/h^2), n = 0..7
-  __device__ __forceinline__ void fill_table2(double2 *tab2, int t) const {
-    if (t < 8) {
-      const double w = t <= 4 ? fma((double)t, w1, w0) : 0.0;
-      tab2[t] = make_double2(w * cs, w * cl);
-    }
-  }
-  // sigma of tet M from one 16-byte lookup; 2 w mu/h^2 = s + s is exact
-  template <int M>
-  __device__ __forceinline__ static void sigma2(const double *Dx, const double *Dy, const double *Dz,
-                                                uint32_t nbits, const double2 *tab2, double (&sg)[6]) {
-    const uint32_t n = (nbits >> (3 * M)) & 7u;
-    const double2 sl = tab2[n];
-    const double s = sl.x, l = sl.y, s2 = s + s;
-    const double lt = l * (Dx[0] + Dy[1] + Dz[2]);
-    sg[0] = fma(s2, Dx[0], lt);
-    sg[1] = fma(s2, Dy[1], lt);
-    sg[2] = fma(s2, Dz[2], lt);
-    sg[3] = s * (Dx[1] + Dy[0]);
-    sg[4] = s * (Dx[2] + Dz[0]);
-    sg[5] = s * (Dy[2] + Dz[1]);
-  }
-
   // the six stress components (xx, yy, zz, xy, xz, yz) of tet M
   template <int M>
   __device__ __forceinline__ static void sigma(const double *Dx, const double *Dy, const double *Dz,
@@ -220,79 +197,6 @@ struct ElastC {
       c[5][q] = (fx01 + fz10) - fy11;
       c[6][q] = (fy01 + fz01) - fx11;
       c[7][q] = (fx11 + fy11) + fz11;
-    }
-  }
-
-  // The same cell with the six tets evaluated one after the other and every
-  // corner formed as soon as its tets are done (each expression keeps the
-  // association of cell(), so the results are bitwise the same): the stresses
-  // of at most three tets are live at a time.  Used by march3e.
-  template <int M>
-  __device__ __forceinline__ static void sigma_t(const double *Dx, const double *Dy, const double *Dz,
-                                                 uint32_t nbits, const double *tab, double (&sg)[6]) {
-    sigma<M>(Dx, Dy, Dz, nbits, tab, sg);
-  }
-  template <int M>
-  __device__ __forceinline__ static void sigma_t(const double *Dx, const double *Dy, const double *Dz,
-                                                 uint32_t nbits, const double2 *tab, double (&sg)[6]) {
-    sigma2<M>(Dx, Dy, Dz, nbits, tab, sg);
-  }
-  template <class TAB>
-  __device__ __forceinline__ void cell_prog(const double (*u)[NIN], uint32_t word, double (*c)[NOUT],
-                                            const TAB *tab) const {
-    const uint32_t nb = valid(word) ? word : 0x3ffffu;
-    constexpr int CX[3] = {0, 3, 4}, CY[3] = {3, 1, 5}, CZ[3] = {4, 5, 2};
-    double X00[3], X10[3], X01[3], X11[3], Y00[3], Y10[3], Y01[3], Y11[3], Z00[3], Z10[3], Z01[3], Z11[3];
-    double s0[6], s1[6], s2[6], s3[6], s4[6], s5[6];
-    double fx00[3], fz11[3], t01[3], fx11[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      X00[q] = u[1][q] - u[0][q]; Y10[q] = u[3][q] - u[1][q]; Z11[q] = u[7][q] - u[3][q];
-      Y11[q] = u[7][q] - u[5][q]; Z10[q] = u[5][q] - u[1][q];
-    }
-    sigma_t<0>(X00, Y10, Z11, nb, tab, s0);
-    sigma_t<1>(X00, Y11, Z10, nb, tab, s1);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      fx00[q] = s0[CX[q]] + s1[CX[q]];
-      c[1][q] = (fx00[q] - s0[CY[q]]) - s1[CZ[q]];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { X10[q] = u[3][q] - u[2][q]; Y00[q] = u[2][q] - u[0][q]; }
-    sigma_t<2>(X10, Y00, Z11, nb, tab, s2);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      fz11[q] = s0[CZ[q]] + s2[CZ[q]];
-      c[3][q] = (s2[CX[q]] + s0[CY[q]]) - fz11[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { X11[q] = u[7][q] - u[6][q]; Z01[q] = u[6][q] - u[2][q]; }
-    sigma_t<3>(X11, Y00, Z01, nb, tab, s3);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double fy00 = s2[CY[q]] + s3[CY[q]];
-      c[2][q] = (fy00 - s2[CX[q]]) - s3[CZ[q]];
-      t01[q] = fx00[q] + fy00;
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { Y01[q] = u[6][q] - u[4][q]; Z00[q] = u[4][q] - u[0][q]; }
-    sigma_t<5>(X11, Y01, Z00, nb, tab, s5);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      fx11[q] = s3[CX[q]] + s5[CX[q]];
-      c[6][q] = (s5[CY[q]] + s3[CZ[q]]) - fx11[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) X01[q] = u[5][q] - u[4][q];
-    sigma_t<4>(X01, Y11, Z00, nb, tab, s4);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double fz00 = s4[CZ[q]] + s5[CZ[q]];
-      const double fy11 = s1[CY[q]] + s4[CY[q]];
-      c[0][q] = -t01[q] - fz00;
-      c[7][q] = (fx11[q] + fy11) + fz11[q];
-      c[4][q] = (fz00 - s4[CX[q]]) - s5[CY[q]];
-      c[5][q] = (s4[CX[q]] + s1[CZ[q]]) - fy11;
     }
   }
 };
@@ -602,7 +506,6 @@ __device__ __forceinline__ void finalize(const MArgs &a, int rhs, const double *
 }  // namespace lsg
 
 #include "march3s.cuh"
-#include "march3e.cuh"
 
 namespace lsg {
 namespace d3 {
@@ -1081,46 +984,11 @@ static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   return check_launch("march3d");
 }
 
-// The lean cubic-cell stencil (march3e.cuh) serves the apply and the PCG
-// stencil of cubic grids; LSG_M3E=0 routes them through march3s (same-box A/B,
-// and the bitwise cross-check of tests/test_gpu_paths.py).
-static bool use_m3e() {
-  static const bool on = [] {
-    const char *e = getenv("LSG_M3E");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-template <int ACT>
-static int launch_e(const ElastC &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
-  static int ctas = -1;
-  constexpr size_t smem = e3::kBytes;
-  if (ctas < 0) {
-    cudaFuncSetAttribute(march3e<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, march3e<ACT>, kThreads, smem) != cudaSuccess)
-      ctas = 2;
-  }
-  dim3 grid;
-  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid, ACT == PCGQ ? 2 : 3);
-  a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
-  if (ACT == PCGQ) {
-    if (launch_pdl(march3e<ACT>, grid, dim3(kThreads), smem, st, ph, g, a) != cudaSuccess)
-      return check_launch("march3e launch");
-  } else {
-    march3e<ACT><<<grid, kThreads, smem, st>>>(ph, g, a);
-  }
-  return check_launch("march3e");
-}
-
 template <int ACT>
 static int dispatch(const lsg_op &op, MArgs a, int k, cudaStream_t st) {
   const Geo g = geo_of(op.grid);
   a.words = static_cast<const uint32_t *>(op.words);
   if (op.kind == LSG_OP_ELASTICITY) {
-    if constexpr (ACT == APPLY || ACT == PCGQ) {
-      if (is_cubic(g) && use_m3e()) return launch_e<ACT>(make_elast_cubic(g, op), g, a, k, st);
-    }
     if (is_cubic(g)) return launch<ElastC, ACT>(make_elast_cubic(g, op), g, a, k, st);
     return launch<Elast, ACT>(make_elast(g, op), g, a, k, st);
   }
