@@ -59,7 +59,9 @@ class Compliance:
 
     # -- state ----------------------------------------------------------------------
     def matrix(self, phi):
-        return self.space.assemble_matrix(fem.elasticity_elements(self.space, self.a_q(phi), self.lame))
+        a_q = self.a_q(phi)
+        return self.space.assemble_matrix_by_parts(
+            lambda part: fem.elasticity_elements(part, a_q[part.sl], self.lame))
 
     def eliminated(self, phi):
         K = self.matrix(phi)
@@ -360,12 +362,15 @@ class Velocity:
         self.grid = grid
         self.space = fem.Space(grid, grid.dim)
         sp_ = self.space
-        elems = stiffness_weight * fem.stiffness_elements(sp_)
-        if mass_weight > 0:
-            elems = elems + mass_weight * fem.mass_elements(sp_)
-        if frozen_chi is not None and frozen_penalty > 0:
-            elems = elems + frozen_penalty * fem.mass_elements(sp_, frozen_chi)
-        B = sp_.assemble_matrix(elems)
+        def form_elements(part):
+            elems = stiffness_weight * fem.stiffness_elements(part)
+            if mass_weight > 0:
+                elems = elems + mass_weight * fem.mass_elements(part)
+            if frozen_chi is not None and frozen_penalty > 0:
+                elems = elems + frozen_penalty * fem.mass_elements(part, np.asarray(frozen_chi)[part.sl])
+            return elems
+
+        B = sp_.assemble_matrix_by_parts(form_elements)
         if boundary_normal_penalty > 0:
             B = B + boundary_normal_penalty * self._normal_matrix()
         self.form_matrix = B.tocsr()

@@ -6,6 +6,7 @@ count" (VERDICT round 1 "pin parity at config size").
     python tests/golden/make_golden_histories.py cfg2_half       # 512x128, all 40 it
     python tests/golden/make_golden_histories.py cfg2_full3      # 1024x256, first 3 it
     python tests/golden/make_golden_histories.py cfg5_half       # 96x48x48, 4 loads, 20 it
+    python tests/golden/make_golden_histories.py cfg5_full1      # 192x96x96, 4 loads, first iteration
 
 Each writes tests/golden/oracle_<name>.npz.  CPU only (tens of minutes to hours:
 the oracle is scipy CSR + scipy ``cg``, single-threaded per solve).  The k load
@@ -44,6 +45,9 @@ JOBS = {
     "cfg2_half": ("cfg2", 2, 40, True),
     "cfg2_full3": ("cfg2", 1, 3, True),
     "cfg5_half": ("cfg5", 2, 20, False),
+    # full size: the oracle assembles its matrices 400k tets at a time
+    # (Space.assemble_matrix_by_parts); ~20 GB resident, ~2 h for one iteration
+    "cfg5_full1": ("cfg5", 1, 1, False),
 }
 
 _SYSTEMS = None

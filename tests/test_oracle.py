@@ -399,3 +399,18 @@ def test_inverse_oracle_matches_reference():
     np.testing.assert_allclose(s1, g["S1"], rtol=1e-9, atol=1e-12 * np.abs(g["S1"]).max())
     vec = derivative_vector(cspace, s1=s1, s0=s0)
     assert rel_l2(vec, g["vec"]) <= 1e-9
+
+
+def test_assembly_by_parts_equals_whole():
+    """The element-chunked assembly (cfg5 at full size does not fit otherwise)
+    gives the matrix of the one-shot assembly, in 2D and 3D."""
+    for lo, hi, n in (((0.0, 0.0), (2.0, 1.0), (6, 4)), ((0.0, 0.0, 0.0), (2.0, 1.0, 1.0), (4, 3, 2))):
+        grid = Grid(lo, hi, n, [])
+        space = fem.Space(grid, grid.dim)
+        rng = np.random.default_rng(3)
+        a_q = rng.uniform(0.1, 1.0, space.quad_weights.shape)
+        whole = space.assemble_matrix(fem.elasticity_elements(space, a_q, (0.6, 0.4)))
+        build = lambda part: fem.elasticity_elements(part, a_q[part.sl], (0.6, 0.4))  # noqa: E731
+        for chunk in (7, 10**6):
+            parts = space.assemble_matrix_by_parts(build, chunk=chunk)
+            assert abs(parts - whole).max() <= 1e-15 * abs(whole).max()
