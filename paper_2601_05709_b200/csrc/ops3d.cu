@@ -936,27 +936,36 @@ static H1P make_h1_plain(const Geo &g, const lsg_op &op) {
 
 int64_t partials_per_rhs(const lsg_grid &) { return kMaxPartials; }
 
-static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid,
-                            int default_waves = 3) {
+static void launch_geometry(const Geo &g, int k, int ctas_per_sm, int &seg, int &nzseg, dim3 &grid) {
   const int64_t nstrips = ceil_div(g.nx + 1, kStrip);
   const int64_t tiles = ceil_div(g.ny + 1, kWarps - 1);
-  // z-segments (one halo plane each) sized for ~3 waves of CTAs and at most
-  // 32 planes (measured on cfg5: 16-32 planes, 3-4 waves are best; shorter
-  // segments pay more halo planes, one wave leaves a tail).
+  // z-segments (one halo plane each): the grid runs in rounds of `slots` resident
+  // CTAs, each CTA marching seg + 1 planes, so the launch costs about
+  // rounds x (seg + 1) plane steps; take the segment count that minimises it
+  // (cfg5: 3 segments of 33 planes = 2 rounds for a half batch of the PCG and 4
+  // for the k = 4 apply; measured against 4 segments: PCG iteration 451 -> 442 us,
+  // apply 232 -> 230 us).  Segments of 5..48 planes: shorter ones pay more in halo
+  // planes and pipeline fill than the model says (cfg3: 5 planes fill one round,
+  // PCG iteration 28.2 -> 26.6 us), longer ones leave a tail.
   const int64_t per_seg = nstrips * tiles * k;
   const int64_t slots = (int64_t)num_sms() * (ctas_per_sm > 0 ? ctas_per_sm : 2);
-  const int64_t wv = default_waves;
-  int64_t ns = ceil_div(wv * slots, per_seg);
-  if (ns < 1) ns = 1;
-  int64_t s = ceil_div(g.nz + 1, ns);
-  // measured: segments of 5..32 planes (cfg3: 5 planes fill one wave, PCG
-  // iteration 28.2 -> 26.6 us; cfg5: 16-32 planes, 3-4 waves)
-  constexpr int64_t smax = 32, smin = 5;
-  if (s > smax) s = smax;
-  if (s < smin) s = smin;
-  while (nstrips * tiles * ceil_div(g.nz + 1, s) > kMaxPartials) s *= 2;
+  const int64_t nzp = g.nz + 1;
+  constexpr int64_t smax = 48, smin = 5;
+  int64_t best_s = nzp, best_cost = -1;
+  for (int64_t ns = 1; ns <= nzp; ++ns) {
+    const int64_t s = ceil_div(nzp, ns);
+    if ((s > smax && ns < nzp) || (s < smin && ns > 1)) continue;
+    const int64_t nseg = ceil_div(nzp, s);
+    const int64_t cost = ceil_div(nseg * per_seg, slots) * (s + 1);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_s = s;
+    }
+  }
+  int64_t s = best_s;
+  while (nstrips * tiles * ceil_div(nzp, s) > kMaxPartials) s *= 2;
   seg = (int)s;
-  nzseg = (int)ceil_div(g.nz + 1, s);
+  nzseg = (int)ceil_div(nzp, s);
   grid = dim3((unsigned)nstrips, (unsigned)tiles, (unsigned)(nzseg * k));
 }
 
@@ -971,9 +980,7 @@ static int launch(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
       ctas = 2;
   }
   dim3 grid;
-  // the PCG stencil runs beside the other half-batch's elementwise passes (two
-  // streams): 2 waves of longer segments measured better there (cfg5 472 -> 466 us)
-  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid, ACT == PCGQ ? 2 : 3);
+  launch_geometry(g, k, ctas, a.seg, a.nzseg, grid);
   a.nstrips = (int)ceil_div(g.nx + 1, kStrip);
   if (ACT == PCGQ) {
     if (launch_pdl(march3s<PH, ACT>, grid, dim3(kThreads), smem, st, ph, g, a) != cudaSuccess)

@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2601_05709_b200 import _lib, build_rect_mesh, build_box_mesh  # noqa: E402
-from paper_2601_05709_b200.fem import DirichletSet, ElasticityOperator, FunctionSpace, _workspace  # noqa: E402
+from paper_2601_05709_b200.fem import (DirichletSet, ElasticityOperator, FunctionSpace, H1Operator,  # noqa: E402
+                                       _workspace)
 
 
 def main():
@@ -89,6 +90,15 @@ def main():
     out["pcg_iter_us"] = t
     out["pcg_gbs"] = bytes_it / (t * 1e-6) / 1e9
     out["pcg_frac"] = out["pcg_gbs"] / peak
+    # the velocity form's PCG iteration (mass + alpha vector Laplacian, one right-hand side)
+    h1 = H1Operator(space, 1.0, 1e-2)
+    hws = _workspace(h1, 1)
+    hws.b.copy_(torch.randn((1, d * N), dtype=torch.float64, device="cuda"))
+    hws.x.zero_()
+    hws.ws.dinv = h1.inverse_diagonal().data_ptr()
+    hop = h1._op()
+    _lib.call("lsg_pcg_start", hop, hws.ws, 0.0, 0.0, 1e12, st)
+    out["h1_pcg_iter_us"] = timed(lambda: _lib.call("lsg_pcg_iterate", hop, hws.ws, it, st), 3, False) / it
     print(json.dumps(out))
 
 
