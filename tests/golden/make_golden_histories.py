@@ -7,6 +7,7 @@ count" (VERDICT round 1 "pin parity at config size").
     python tests/golden/make_golden_histories.py cfg2_full3      # 1024x256, first 3 it
     python tests/golden/make_golden_histories.py cfg5_half       # 96x48x48, 4 loads, 20 it
     python tests/golden/make_golden_histories.py cfg5_full1      # 192x96x96, 4 loads, first iteration
+    python tests/golden/make_golden_histories.py cfg5_full3      # 192x96x96, 4 loads, first 3 iterations
 
 Each writes tests/golden/oracle_<name>.npz.  CPU only (tens of minutes to hours:
 the oracle is scipy CSR + scipy ``cg``, single-threaded per solve).  The k load
@@ -48,6 +49,7 @@ JOBS = {
     # full size: the oracle assembles its matrices 400k tets at a time
     # (Space.assemble_matrix_by_parts); ~20 GB resident, ~2 h for one iteration
     "cfg5_full1": ("cfg5", 1, 1, False),
+    "cfg5_full3": ("cfg5", 1, 3, False),  # warm-started solves on a transported level set (~3 h)
 }
 
 _SYSTEMS = None

@@ -11,7 +11,8 @@ as fixtures (tests/golden/make_golden_histories.py):
   patches and support strips), all 40 iterations;
 * cfg2 at full size (1024x256), the first 3 iterations;
 * cfg5 at full size (192x96x96, 5.4M dofs, 4 load cases), the first iteration
-  (the oracle assembles its matrices 400k tets at a time).
+  and, when generated, the first three (the oracle assembles its matrices 400k
+  tets at a time).
 
 Per iteration: J, C, the Lagrangian and B(theta, theta) within 1e-4 relative
 and identical discrete counters (RNG-driven transport steps, CFL substeps,
@@ -37,7 +38,7 @@ from paper_2601_05709_b200.fem import solve_batched  # noqa: E402
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 # fixture -> (config, scale)
 FIXTURES = {"cfg3": ("cfg3", 1), "cfg5_half": ("cfg5", 2), "cfg2_half": ("cfg2", 2), "cfg2_full3": ("cfg2", 1),
-            "cfg5_full1": ("cfg5", 1)}
+            "cfg5_full1": ("cfg5", 1), "cfg5_full3": ("cfg5", 1)}
 
 
 def _fixture(name):
