@@ -9,7 +9,7 @@ for v in "$@"; do
   lib=${lib:-paper_2601_05709_b200/liblsgpu.so}
   for g in ${GRIDS:-192x96x96,4,20 96x48x48,1,100}; do
     IFS=',' read -r G K IT <<< "$g"
-    echo "$label $G k=$K: $(env $envs LSG_LIB_PATH=$PWD/$lib timeout 300 python tools/kbench.py --grid $G --k $K --iters $IT 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("apply %.1f us (%.3f)  pcg %.1f us  h1 %.1f us" % (d["apply_clean_us"], d["apply_clean_frac"], d["pcg_iter_us"], d.get("h1_pcg_iter_us", 0)))')" >> gpurun_out/ab.log
+    echo "$label $G k=$K: $(env $envs LSG_LIB_PATH=$PWD/$lib timeout 300 python tools/kbench.py --grid $G --k $K --iters $IT $KBENCH_ARGS 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("apply %.1f us (%.3f)  pcg %.1f us  h1 %.1f us" % (d["apply_clean_us"], d["apply_clean_frac"], d["pcg_iter_us"], d.get("h1_pcg_iter_us", 0)))')" >> gpurun_out/ab.log
   done
 done
 done

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--grid", default="1024x256")
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--phi", default="random", choices=("random", "smooth"),
+                    help="material: per-node random phi (every cell mixed) or cfg5's periodic holes")
     args = ap.parse_args()
     n = tuple(int(v) for v in args.grid.split("x"))
     if len(n) == 2:
@@ -39,7 +41,11 @@ def main():
         lame = (0.576923, 0.384615)
     d, N, E, k = mesh.dim, mesh.num_vertices, mesh.num_elements, args.k
     space = FunctionSpace(mesh, d)
-    phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
+    if args.phi == "smooth":
+        v = mesh.vertices if isinstance(mesh.vertices, np.ndarray) else mesh.vertices.cpu().numpy()
+        phi = torch.as_tensor(-np.prod(np.cos(6 * np.pi * v), axis=1) - 0.3, device="cuda")
+    else:
+        phi = torch.as_tensor(np.random.default_rng(0).standard_normal(N), device="cuda")
     op = ElasticityOperator(space, phi, lame, 1e-3, DirichletSet.on_tags(space, 1))
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
