@@ -49,7 +49,8 @@ JOBS = {
     # full size: the oracle assembles its matrices 400k tets at a time
     # (Space.assemble_matrix_by_parts); ~20 GB resident, ~2 h for one iteration
     "cfg5_full1": ("cfg5", 1, 1, False),
-    "cfg5_full3": ("cfg5", 1, 3, False),  # warm-started solves on a transported level set (~3 h)
+    "cfg5_full3": ("cfg5", 1, 3, False),  # warm-started solves on a transported level set (~2 h)
+    "cfg5_full5": ("cfg5", 1, 5, False),  # ... through the first reinitialisation (~3 h)
 }
 
 _SYSTEMS = None
@@ -86,18 +87,28 @@ def main(name):
     om.solve_states = parallel_states(om)
     t0 = time.time()
 
+    keys = ("cost", "lagrangian", "form_value", "t_end", "steps", "nsub_transport", "nsub_reinit")
+    done = []
+
+    def save(rows):
+        out = {k: np.array([r[k] for r in rows]) for k in keys}
+        out["constraint"] = np.array([r["constraint"][0] for r in rows])
+        out["cg_iters"] = np.array([r["cg_iters"] for r in rows])
+        out["grid"] = np.array(c.n)
+        np.savez_compressed(os.path.join(HERE, f"oracle_{name}.npz"), **out)
+        return out
+
     def on_record(rec, phi):
         print(f"[{name}] it {rec['iteration']:3d}  J={rec['cost']:.10e}  C={rec['constraint'][0]:.10e}  "
               f"cg={sum(rec['cg_iters'])}  steps={rec['steps']}  nsub={rec['nsub_transport']}/"
               f"{rec['nsub_reinit']}  {time.time() - t0:.0f}s", flush=True)
+        # every completed iteration is a valid fixture (a run of n iterations is the
+        # prefix of a longer one): keep the file current, a long job can be cut short
+        done.append(dict(rec))
+        save(done)
 
     _, hist = odriver.run(om, ovel, ophi, oparams, h, on_record=on_record)
-    keys = ("cost", "lagrangian", "form_value", "t_end", "steps", "nsub_transport", "nsub_reinit")
-    out = {k: np.array([r[k] for r in hist]) for k in keys}
-    out["constraint"] = np.array([r["constraint"][0] for r in hist])
-    out["cg_iters"] = np.array([r["cg_iters"] for r in hist])
-    out["grid"] = np.array(c.n)
-    np.savez_compressed(os.path.join(HERE, f"oracle_{name}.npz"), **out)
+    out = save(hist)
     print(name, len(hist), out["cost"][[0, -1]], f"{time.time() - t0:.0f}s")
 
 

@@ -38,7 +38,7 @@ from paper_2601_05709_b200.fem import solve_batched  # noqa: E402
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 # fixture -> (config, scale)
 FIXTURES = {"cfg3": ("cfg3", 1), "cfg5_half": ("cfg5", 2), "cfg2_half": ("cfg2", 2), "cfg2_full3": ("cfg2", 1),
-            "cfg5_full1": ("cfg5", 1), "cfg5_full3": ("cfg5", 1)}
+            "cfg5_full1": ("cfg5", 1), "cfg5_full3": ("cfg5", 1), "cfg5_full5": ("cfg5", 1)}
 
 
 def _fixture(name):
