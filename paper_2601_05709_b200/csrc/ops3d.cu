@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kEwThreads)
     for (int u = 0; u < 4; ++u) {
       const int64_t t = base + u * stride;
       if (t < n) {
-        Q[u] = __ldg(q + off + t);
+        Q[u] = __ldcs(q + off + t);  // q is dead after this pass: evict-first keeps p and r in L2
         D[u] = __ldg(dinv + t);
         R[u] = r[off + t];
       }
