@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, LSG_M3_MINB) march3s(PH ph, Geo g, M
       for (int q = 0; q < 3; ++q) yv[q] = ((m >> q) & 1u) ? raw[q] : accv[q];
       if constexpr (ACT == APPLY) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) a.y[voff + node * 3 + q] = yv[q];
+        for (int q = 0; q < 3; ++q) __stcs(a.y + voff + node * 3 + q, yv[q]);  // not re-read here: keep x in L2
       } else if constexpr (ACT == RESID) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
