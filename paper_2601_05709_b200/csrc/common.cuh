@@ -23,6 +23,8 @@ constexpr int kWarp = 32;
 // SM count of the current device (queried once per device): grids are sized in
 // multiples of it, and a cooperative grid may not exceed it times the CTAs per SM.
 int num_sms();
+// L2 capacity of the current device in bytes (queried once per device).
+int64_t l2_bytes();
 
 // Programmatic dependent launch (PDL) for the PCG-iteration kernels: a kernel
 // launched with launch_pdl may have its CTAs scheduled while its predecessor

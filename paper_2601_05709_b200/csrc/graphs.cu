@@ -82,6 +82,19 @@ int num_sms() {
   return cache[dev];
 }
 
+int64_t l2_bytes() {
+  constexpr int kMaxDev = 64;
+  static int64_t cache[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 126ll << 20;
+  if (cache[dev] <= 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) != cudaSuccess || v <= 0) v = 126 << 20;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
 // 3D rotates three direction buffers (phase = iteration index mod 3), 2D two
 void advance_parity(const lsg_op &op, lsg_pcg_ws &ws, int niter) {
   if (op.grid.dim == 3) ws.parity = (ws.parity + niter) % 3;

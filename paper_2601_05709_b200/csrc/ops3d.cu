@@ -513,6 +513,28 @@ namespace d3 {
 // ---------------------------------------------------------------------------
 // Elementwise kernels
 // ---------------------------------------------------------------------------
+// M^-1 is read by both elementwise passes of every right-hand side (8 times per
+// cfg5 iteration).  When the batch is far larger than L2 the passes ask L2 to
+// evict it last (cfg5 PCG iteration 439.6 -> 434.0 us); batches near the L2
+// size measured ~0.7% slower with the hint, so they keep the normal priority.
+template <bool KEEP>
+__device__ __forceinline__ uint64_t l2_policy() {
+  uint64_t pol = 0;
+  if constexpr (KEEP) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+template <bool KEEP>
+__device__ __forceinline__ double ld_policy(const double *p, uint64_t pol) {
+  if constexpr (KEEP) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
+
+template <bool KEEP>
 __global__ void __launch_bounds__(kEwThreads)
     pcg_update(int64_t n, const double *dinv, double *r, const double *q, lsg_pcg_scalars *scal,
                double *partials, uint32_t *counters) {
@@ -524,6 +546,7 @@ __global__ void __launch_bounds__(kEwThreads)
   const double alpha = s.alpha;
   const size_t off = (size_t)rhs * (size_t)n;
   double part[2] = {0.0, 0.0};
+  const uint64_t pol = l2_policy<KEEP>();
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
     double Q[4], R[4], D[4];
@@ -532,7 +555,7 @@ __global__ void __launch_bounds__(kEwThreads)
       const int64_t t = base + u * stride;
       if (t < n) {
         Q[u] = __ldcs(q + off + t);  // q is dead after this pass: evict-first keeps p and r in L2
-        D[u] = __ldg(dinv + t);
+        D[u] = ld_policy<KEEP>(dinv + t, pol);
         R[u] = r[off + t];
       }
     }
@@ -573,6 +596,7 @@ __global__ void __launch_bounds__(kEwThreads)
 // read and written every second iteration only).  The stencil half
 // (march3s<PH, PCGQ>) then reads only p.  Used in 3D, where a fused pass A is
 // fp64-issue-bound.
+template <bool KEEP>
 __global__ void __launch_bounds__(kEwThreads, 4)  // 4 CTAs/SM: the grid is one full wave
     pcg_prep(int64_t n, const double *dinv, const double *r, const double *p_old,
              const double *p_old2, double *p_new, double *x, const lsg_pcg_scalars *scal) {
@@ -584,6 +608,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)  // 4 CTAs/SM: the grid is one 
   const int it = (int)s.iters;
   const bool upd = it >= 2 && (it & 1) == 0;
   const size_t off = (size_t)rhs * (size_t)n;
+  const uint64_t pol = l2_policy<KEEP>();
   const int64_t stride = (int64_t)gridDim.x * kEwThreads;
   for (int64_t base = (int64_t)blockIdx.x * kEwThreads + threadIdx.x; base < n; base += 4 * stride) {
     double R[4], P[4], D[4], X[4], P2[4];
@@ -593,7 +618,7 @@ __global__ void __launch_bounds__(kEwThreads, 4)  // 4 CTAs/SM: the grid is one 
       if (t < n) {
         R[u] = __ldg(r + off + t);
         P[u] = __ldg(p_old + off + t);
-        D[u] = __ldg(dinv + t);
+        D[u] = ld_policy<KEEP>(dinv + t, pol);
         if (upd) {
           X[u] = x[off + t];
           P2[u] = __ldg(p_old2 + off + t);
@@ -1061,7 +1086,7 @@ int pcg_start(const lsg_op &op, lsg_pcg_ws &ws, double rtol, double atol, double
 // One 3D PCG iteration (elementwise p-pass, stencil q = A p, update) of a
 // batch of right-hand sides; `after_prep` is recorded once the p-pass is queued.
 static int iterate_once(const lsg_op &op, const lsg_pcg_ws &ws, int parity, int64_t n, dim3 eg,
-                        cudaStream_t st, cudaEvent_t after_prep) {
+                        cudaStream_t st, cudaEvent_t after_prep, int keep_dinv) {
   MArgs a = {};
   a.y = ws.q;
   a.dinv = ws.dinv;
@@ -1072,8 +1097,8 @@ static int iterate_once(const lsg_op &op, const lsg_pcg_ws &ws, int parity, int6
   const int ph = parity;  // iteration index mod 3 = slot of the new direction
   double *p_new = ring[ph], *p_old = ring[ph == 0 ? 2 : ph - 1];
   double *p_old2 = ring[ph == 2 ? 0 : ph + 1];
-  if (launch_pdl(pcg_prep, eg, dim3(kEwThreads), 0, st, n, ws.dinv, (const double *)ws.r,
-                 (const double *)p_old, (const double *)p_old2, p_new, ws.x,
+  if (launch_pdl(keep_dinv ? pcg_prep<true> : pcg_prep<false>, eg, dim3(kEwThreads), 0, st, n, ws.dinv,
+                 (const double *)ws.r, (const double *)p_old, (const double *)p_old2, p_new, ws.x,
                  (const lsg_pcg_scalars *)ws.scal) != cudaSuccess)
     return check_launch("pcg_prep3d launch");
   int rc = check_launch("pcg_prep3d");
@@ -1082,8 +1107,8 @@ static int iterate_once(const lsg_op &op, const lsg_pcg_ws &ws, int parity, int6
   a.x = p_new;
   rc = dispatch<PCGQ>(op, a, ws.k, st);
   if (rc) return rc;
-  if (launch_pdl(pcg_update, eg, dim3(kEwThreads), 0, st, n, ws.dinv, ws.r, (const double *)ws.q,
-                 ws.scal, ws.partials, ws.counters) != cudaSuccess)
+  if (launch_pdl(keep_dinv ? pcg_update<true> : pcg_update<false>, eg, dim3(kEwThreads), 0, st, n, ws.dinv,
+                 ws.r, (const double *)ws.q, ws.scal, ws.partials, ws.counters) != cudaSuccess)
     return check_launch("pcg_update3d launch");
   return check_launch("pcg_update3d");
 }
@@ -1131,6 +1156,9 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     if (slots < 1) slots = 1;
     return dim3((unsigned)(need < slots ? need : slots), (unsigned)k);
   };
+  // seven vectors per right-hand side move per iteration; the M^-1 hint pays when
+  // they exceed L2 several times over
+  const int keep_dinv = (int64_t)ws.k * n * 8 * 7 > 4 * l2_bytes() ? 1 : 0;
   if (streams3d() == 2 && ws.k >= 2) {
     // library-owned second stream and events, one set per device
     constexpr int kMaxDev = 64;
@@ -1153,10 +1181,10 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
     if (cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(st2, ev_fork, 0) != cudaSuccess)
       return check_launch("pcg3d fork");
     for (int it = 0; it < niter; ++it) {
-      int rc = iterate_once(op, w1, ws.parity, n, g1, st, ev_prep);
+      int rc = iterate_once(op, w1, ws.parity, n, g1, st, ev_prep, keep_dinv);
       if (rc) return rc;
       if (cudaStreamWaitEvent(st2, ev_prep, 0) != cudaSuccess) return check_launch("pcg3d wait");
-      rc = iterate_once(op, w2, ws.parity, n, g2, st2, nullptr);
+      rc = iterate_once(op, w2, ws.parity, n, g2, st2, nullptr, keep_dinv);
       if (rc) return rc;
       ws.parity = ws.parity == 2 ? 0 : ws.parity + 1;
     }
@@ -1166,7 +1194,7 @@ int pcg_iterate(const lsg_op &op, lsg_pcg_ws &ws, int niter, cudaStream_t st) {
   }
   const dim3 eg = grid_for(ws.k);
   for (int it = 0; it < niter; ++it) {
-    int rc = iterate_once(op, ws, ws.parity, n, eg, st, nullptr);
+    int rc = iterate_once(op, ws, ws.parity, n, eg, st, nullptr, keep_dinv);
     if (rc) return rc;
     ws.parity = ws.parity == 2 ? 0 : ws.parity + 1;
   }
