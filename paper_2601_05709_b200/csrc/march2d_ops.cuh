@@ -731,7 +731,7 @@ __device__ __forceinline__ void cp_async_wait_all_but() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <class PH, int A>
+template <class PH, int A, bool FIRST>
 __device__ __forceinline__ void march_pcg_rqs(const PH &ph, const Geo &g, const MArgs &a, int bx,
                                               int by, int rhs, double beta, double alpha_prev,
                                               double (&part)[5], double *ring) {
@@ -769,12 +769,32 @@ __device__ __forceinline__ void march_pcg_rqs(const PH &ph, const Geo &g, const 
     if constexpr (NC == 2) cp_async16(dst, src);
     else cp_async8(dst, src);
   };
+  // FIRST: r_{i-1} and p_{i-1} are dead once this pass has read them; when the new
+  // r_i, p_i of the whole batch fit in L2 beside them (and the six vectors do not),
+  // copying them with an evict-first policy leaves L2 to the vectors the next pass
+  // reads (cfg2: 49.9 -> 46.9 us).  It loses on larger systems (cfg4: 176 -> 196 us), so
+  // the launcher decides (launch_pcg_rq).
+  uint64_t pol_first = 0;
+  if constexpr (FIRST) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+  auto cpy_dead = [&](double *dst, const double *src) {
+    if constexpr (FIRST) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      if constexpr (NC == 2)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src),
+                     "l"(pol_first));
+      else
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src),
+                     "l"(pol_first));
+    } else {
+      cpy(dst, src);
+    }
+  };
   // issue the copies of row r into slot sl (one commit group per row)
   auto fetch = [&](int r, int sl) {
     double *S = myring + sl * RG::SLOT;
     const int64_t node = (int64_t)r * nxp + ic;
-    cpy(S + 0 * FS + lane * NC, p_in + node * NC);
-    cpy(S + 1 * FS + lane * NC, r_in + node * NC);
+    cpy_dead(S + 0 * FS + lane * NC, p_in + node * NC);
+    cpy_dead(S + 1 * FS + lane * NC, r_in + node * NC);
     cpy(S + 2 * FS + lane * NC, a.dinv + node * NC);
     if (own && r >= J0 && r < J1) cpy(S + 3 * FS + lane * NC, xs + node * NC);
     uint32_t *W = reinterpret_cast<uint32_t *>(S + 4 * FS);
@@ -938,7 +958,7 @@ __device__ __forceinline__ void march_pcg_rqs(const PH &ph, const Geo &g, const 
 // No minimum-blocks bound: ptxas settles at 122 registers (4 CTAs/SM).  Measured
 // against it: a minBlocks of 1 (176 registers, 2 CTAs/SM) 9-13% slower, 5
 // (96 registers, small spills) 3-8% slower, 6 (80 registers) 30% slower.
-template <class PH, int A>
+template <class PH, int A, bool FIRST>
 __global__ void __launch_bounds__(kThreads) march_pcg_rqs_kernel(PH ph, Geo g, MArgs a) {
   constexpr int NP = 5;
   __shared__ double scratch[NP * kWarps];
@@ -950,7 +970,7 @@ __global__ void __launch_bounds__(kThreads) march_pcg_rqs_kernel(PH ph, Geo g, M
   double part[NP];
 #pragma unroll
   for (int t = 0; t < NP; ++t) part[t] = 0.0;
-  march_pcg_rqs<PH, A>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.beta, s.alpha, part, ring);
+  march_pcg_rqs<PH, A, FIRST>(ph, g, a, blockIdx.x, blockIdx.y, rhs, s.beta, s.alpha, part, ring);
   const int nblk = gridDim.x * gridDim.y;
   const int blk = blockIdx.y * gridDim.x + blockIdx.x;
   double tot[NP];

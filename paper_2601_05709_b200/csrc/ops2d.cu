@@ -313,11 +313,11 @@ static bool pcg_rq_on() {
   return v == 1;
 }
 
-template <class PH, int A>
-static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+template <class PH, int A, bool FIRST>
+static int launch_pcg_rq_hint(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
   static int ctas_per_sm = -1;
   if (ctas_per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH, A>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, march_pcg_rqs_kernel<PH, A, FIRST>,
                                                       kThreads, 0) != cudaSuccess)
       ctas_per_sm = 4;
   }
@@ -325,9 +325,22 @@ static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_
   a.seg = seg_for(g, k, ctas_per_sm, a.nstrips);
   const dim3 grid((unsigned)ceil_div(a.nstrips, kWarps), (unsigned)ceil_div(g.ny + 1, a.seg),
                   (unsigned)k);
-  if (launch_pdl(march_pcg_rqs_kernel<PH, A>, grid, dim3(kThreads), 0, st, ph, g, a) != cudaSuccess)
+  if (launch_pdl(march_pcg_rqs_kernel<PH, A, FIRST>, grid, dim3(kThreads), 0, st, ph, g, a) != cudaSuccess)
     return check_launch("march2d_pcg_rq launch");
   return check_launch("march2d_pcg_rq");
+}
+
+template <class PH, int A>
+static int launch_pcg_rq(const PH &ph, const Geo &g, MArgs a, int k, cudaStream_t st) {
+  // evict-first copies of the dead r_{i-1}, p_{i-1} (march_pcg_rqs): for batches whose six
+  // vectors overflow L2 while the two new ones fit in it with room to spare.  Measured
+  // (off -> on): cfg2 1024x256 k=8 49.9 -> 46.9 us, 1024x512 k=4 50.5 -> 48.2, k=6 38.8 ->
+  // 38.2; outside the band it loses (k=10 62.9 -> 66.1, k=12 73.3 -> 78.4, cfg4 176 -> 196),
+  // and so does a single field of the same size (2048x1024 k=1 49.9 -> 52.4).
+  const int64_t vec = (int64_t)k * (g.nx + 1) * (g.ny + 1) * PH::NC * 8;
+  const bool first = k >= 4 && 6 * vec > l2_bytes() && 10 * vec <= 3 * l2_bytes();
+  return first ? launch_pcg_rq_hint<PH, A, true>(ph, g, a, k, st)
+               : launch_pcg_rq_hint<PH, A, false>(ph, g, a, k, st);
 }
 
 template <class PH>
